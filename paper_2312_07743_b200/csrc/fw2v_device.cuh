@@ -1,0 +1,48 @@
+// Device-side data types shared by the FULL-W2V B200 kernels and the host
+// runtime. Plain structs only (they cross the host/device launch boundary).
+#pragma once
+
+#include <cstdint>
+
+namespace fw2v {
+
+// One batch of post-subsampling sentences resident in HBM.
+//   ids      [W]        kept token ids of all sentences, concatenated
+//   offsets  [S+1]      sentence boundaries into ids (word units)
+//   negs     [W*N]      N negatives per target position (position-major)
+//   alpha    [S]        per-sentence learning rate (lr_at before the sentence)
+struct BatchView {
+    const int32_t* ids;
+    const uint32_t* offsets;
+    const int32_t* negs;
+    const float* alpha;
+    int32_t n_sentences;
+};
+
+// Embedding matrices in HBM: row w of syn0 (reference `input`, context side)
+// at syn0 + w*stride, same for syn1 (reference `output`, target/negative
+// side). stride >= dim; columns dim..stride-1 are zero and stay zero.
+struct ModelView {
+    float* syn0;
+    float* syn1;
+    int32_t dim;
+    int32_t stride;
+    int32_t vocab;
+};
+
+// Device-side instrumented access counters, in the reference's units
+// (whole-vector accesses, traffic.hpp:19-40).
+struct DevCounters {
+    unsigned long long context_reads;
+    unsigned long long context_writes;
+    unsigned long long sample_reads;
+    unsigned long long sample_writes;
+    unsigned long long ring_hits;
+    unsigned long long words;
+    unsigned long long sentences;
+    unsigned long long pad;
+};
+
+enum ReuseMode : int32_t { kLifetime = 0, kWindow = 1, kNone = 2, kWindowSnapshot = 3 };
+
+} // namespace fw2v

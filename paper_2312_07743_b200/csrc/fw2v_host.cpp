@@ -1,0 +1,1041 @@
+// Host runtime of the B200 FULL-W2V trainer: the C-ABI declared in
+// include/fw2v.h.
+//
+// Structure (SURVEY.md §1 "new framework layer map"):
+//   H1 batching threads — one per producer p (reference producers,
+//      trainer.cpp:429-462). Each owns a contiguous sentence chunk, assembles
+//      batches (subsampling + precomputed negatives, sampler.cpp:41-63) with the
+//      reference's RNG stream derive(seed, epoch, p, k) straight into pinned
+//      buffers, stamps per-sentence alpha from a global word reservation
+//      (lr_at, model.cpp:39), copies H2D and launches on its own CUDA stream.
+//      Two pinned/device buffer slots per producer double-buffer the pipeline.
+//   H2 this C-ABI — plain pointers, int status, thread-local last error.
+//   D0 kernels in fw2v_kernels.cu (K1 Hogwild lifetime, K2 exact serial).
+// There is no CPU training path: without a CUDA device every training entry
+// point fails with FW2V_ERR_NO_DEVICE.
+#include "fw2v.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <ctime>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fw2v_device.cuh"
+
+namespace fw2v {
+cudaError_t launch_k1(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf,
+                      bool fast, DevCounters* ctr, cudaStream_t st);
+bool k1_shape_supported(int lanes, int vec);
+cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf, int mode, bool serial,
+                      DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st);
+} // namespace fw2v
+
+namespace {
+
+using namespace fw2v;
+
+thread_local std::string g_error;
+
+struct Failure {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
+
+#define FW2V_CK(expr)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            fail(FW2V_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FW2V_OK;
+    } catch (const Failure& e) {
+        g_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_error = "host allocation failed";
+        return FW2V_ERR_BAD_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return FW2V_ERR_BAD_ARGUMENT;
+    }
+}
+
+// ------------------------------------------------------------------ RNG
+// splitmix64 streams, identical to ringvec::Rng (rng.hpp:11-45).
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+struct Rng {
+    uint64_t state;
+    static Rng derive(uint64_t seed, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
+        Rng r{mix64(seed)};
+        r.state = mix64(r.state ^ mix64(a + kGolden));
+        r.state = mix64(r.state ^ mix64(b + 0xbf58476d1ce4e5b9ULL));
+        r.state = mix64(r.state ^ mix64(c + 0x94d049bb133111ebULL));
+        return r;
+    }
+    inline uint64_t next() {
+        state += kGolden;
+        return mix64(state);
+    }
+    inline double next_double() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+
+double thread_cpu_seconds() {
+    timespec ts{};
+    clock_gettime(CLOCK_THREAD_CPUTIME_ID, &ts);
+    return static_cast<double>(ts.tv_sec) + 1e-9 * static_cast<double>(ts.tv_nsec);
+}
+
+double wall_seconds() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------ samplers
+// subsample_keep_probs (corpus.cpp:215-230)
+bool keep_probs(const uint64_t* counts, int32_t v, double t, double* out) {
+    if (t <= 0.0) return false;
+    uint64_t tot = 0;
+    for (int32_t w = 0; w < v; ++w) tot += counts[w];
+    const double total = static_cast<double>(tot);
+    for (int32_t w = 0; w < v; ++w) {
+        const double f = static_cast<double>(counts[w]) / total;
+        double p = 1.0;
+        if (f > 0.0) {
+            p = (std::sqrt(f / t) + 1.0) * (t / f);
+            if (p > 1.0) p = 1.0;
+        }
+        out[w] = p;
+    }
+    return true;
+}
+
+// NegativeTable::build (sampler.cpp:9-35): slot s -> first w whose cumulative
+// count^power bracket contains the slot midpoint.
+void build_table(const uint64_t* counts, int32_t v, double power, uint64_t size, int32_t* slots) {
+    if (size < static_cast<uint64_t>(v)) fail(FW2V_ERR_BAD_ARGUMENT, "table_size must be >= |V|");
+    if (power < 0.0) fail(FW2V_ERR_BAD_ARGUMENT, "power must be >= 0");
+    std::vector<double> cum(static_cast<size_t>(v));
+    double total = 0.0;
+    for (int32_t w = 0; w < v; ++w) {
+        total += std::pow(static_cast<double>(counts[w]), power);
+        cum[static_cast<size_t>(w)] = total;
+    }
+    size_t w = 0;
+    for (uint64_t s = 0; s < size; ++s) {
+        const double mid = (static_cast<double>(s) + 0.5) / static_cast<double>(size) * total;
+        while (w + 1 < static_cast<size_t>(v) && mid >= cum[w]) ++w;
+        slots[s] = static_cast<int32_t>(w);
+    }
+}
+
+// Walker alias table over count^power (throughput sampler, north_star
+// "unigram^0.75 alias table"): one 64-bit draw -> column (Lemire
+// multiply-high) + 32-bit coin.
+struct AliasTable {
+    std::vector<uint32_t> prob;  // threshold in 2^32 units
+    std::vector<int32_t> alias;
+    uint32_t n = 0;
+    void build(const uint64_t* counts, int32_t v, double power) {
+        n = static_cast<uint32_t>(v);
+        std::vector<double> p(static_cast<size_t>(v));
+        double total = 0.0;
+        for (int32_t w = 0; w < v; ++w) total += (p[static_cast<size_t>(w)] = std::pow(static_cast<double>(counts[w]), power));
+        std::vector<int32_t> small, large;
+        for (int32_t w = 0; w < v; ++w) {
+            p[static_cast<size_t>(w)] *= static_cast<double>(v) / total;
+            (p[static_cast<size_t>(w)] < 1.0 ? small : large).push_back(w);
+        }
+        prob.assign(static_cast<size_t>(v), 0xffffffffu);
+        alias.resize(static_cast<size_t>(v));
+        for (int32_t w = 0; w < v; ++w) alias[static_cast<size_t>(w)] = w;
+        while (!small.empty() && !large.empty()) {
+            const int32_t s = small.back(), l = large.back();
+            small.pop_back();
+            const double ps = p[static_cast<size_t>(s)];
+            prob[static_cast<size_t>(s)] = static_cast<uint32_t>(std::min(4294967295.0, ps * 4294967296.0));
+            alias[static_cast<size_t>(s)] = l;
+            p[static_cast<size_t>(l)] -= 1.0 - ps;
+            if (p[static_cast<size_t>(l)] < 1.0) {
+                large.pop_back();
+                small.push_back(l);
+            }
+        }
+    }
+    inline int32_t sample(uint64_t u) const {
+        const uint32_t col = static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(u)) * n) >> 32);
+        return static_cast<uint32_t>(u >> 32) < prob[col] ? static_cast<int32_t>(col) : alias[col];
+    }
+};
+
+// lr_at (model.cpp:39-45)
+inline float lr_at(uint64_t trained, uint64_t total, float alpha0) {
+    const double progress = static_cast<double>(trained) / static_cast<double>(total);
+    const double a = static_cast<double>(alpha0) * (1.0 - progress);
+    const double floor_ = static_cast<double>(alpha0) * 1e-4;
+    return static_cast<float>(std::max(a, floor_));
+}
+
+// analytic_traffic (traffic.cpp:21-59)
+void analytic(uint64_t len, int width, int neg, int mode, uint64_t* t) {
+    uint64_t pairs = 0;
+    if (len >= 2) {
+        const uint64_t g = std::min<uint64_t>(static_cast<uint64_t>(width), len - 1);
+        pairs = 2 * g * len - g * (g + 1);
+    }
+    const uint64_t samples = static_cast<uint64_t>(neg) + 1;
+    const uint64_t windows = len >= 2 ? len : 0;
+    switch (mode) {
+    case kLifetime:
+    case kWindowSnapshot:
+        t[0] = len; t[1] = len; t[2] = windows * samples; t[3] = windows * samples;
+        t[4] = windows > 0 ? samples * pairs - len : 0;
+        break;
+    case kWindow:
+        t[0] = pairs; t[1] = pairs; t[2] = windows * samples; t[3] = windows * samples;
+        t[4] = static_cast<uint64_t>(neg) * pairs;
+        break;
+    default:
+        t[0] = samples * pairs; t[1] = samples * pairs; t[2] = samples * pairs;
+        t[3] = samples * pairs; t[4] = 0;
+        break;
+    }
+}
+
+// ----------------------------------------------------------- batch assembly
+struct CorpusView {
+    const uint64_t* offsets;
+    const int32_t* ids;
+    uint64_t n;
+};
+
+struct Sampler {
+    const double* keep = nullptr;     // null: subsampling off
+    const int32_t* slots = nullptr;   // reference table
+    uint64_t table_size = 0;
+    const AliasTable* alias = nullptr;  // non-null: alias sampler
+    int n_neg = 0;
+};
+
+struct BatchOut {
+    int32_t* ids;
+    uint32_t* offsets;  // relative, kept+1 entries
+    int32_t* negs;
+    uint64_t cap_words;
+    uint64_t cap_sentences;
+};
+
+// assemble_batch (sampler.cpp:41-63) + subsample_sentence (corpus.cpp:232-241):
+// same RNG consumption order, so the batch equals the reference's for the
+// same stream. Returns kept sentences; *words = their total length.
+uint64_t assemble(const CorpusView& c, uint64_t& cursor, uint64_t end, uint64_t max_sentences,
+                  const Sampler& sp, Rng& rng, const BatchOut& out, uint64_t* words) {
+    uint64_t kept = 0, w = 0;
+    out.offsets[0] = 0;
+    const int n_neg = sp.n_neg;
+    while (kept < max_sentences && cursor < end) {
+        const uint64_t b = c.offsets[cursor], e = c.offsets[cursor + 1];
+        if (w + (e - b) > out.cap_words) break;  // caller sized for the worst case; never hit
+        const uint64_t start = w;
+        if (sp.keep != nullptr) {
+            for (uint64_t p = b; p < e; ++p) {
+                const int32_t id = c.ids[p];
+                if (rng.next_double() < sp.keep[id]) out.ids[w++] = id;
+            }
+        } else {
+            std::memcpy(out.ids + w, c.ids + b, sizeof(int32_t) * (e - b));
+            w += e - b;
+        }
+        ++cursor;
+        if (w == start) continue;
+        int32_t* ng = out.negs + start * static_cast<uint64_t>(n_neg);
+        const uint64_t cnt = (w - start) * static_cast<uint64_t>(n_neg);
+        if (sp.alias != nullptr) {
+            for (uint64_t x = 0; x < cnt; ++x) ng[x] = sp.alias->sample(rng.next());
+        } else {
+            const uint64_t ts = sp.table_size;
+            for (uint64_t x = 0; x < cnt; ++x) ng[x] = sp.slots[rng.next() % ts];
+        }
+        ++kept;
+        out.offsets[kept] = static_cast<uint32_t>(w);
+    }
+    *words = w;
+    return kept;
+}
+
+// ------------------------------------------------------------ K1 shapes
+struct Shape {
+    int lanes = 0, vec = 0;
+};
+
+Shape choose_shape(int dim, int lanes_pref) {
+    static const Shape table[] = {{4, 1},  {4, 2},  {4, 4},   {8, 4},   {16, 4},  {32, 4},
+                                  {32, 6}, {32, 8}, {32, 10}, {32, 12}, {32, 16}};
+    if (lanes_pref > 0) {
+        static const int vecs[] = {1, 2, 4, 6, 8, 10, 12, 16};
+        for (int v : vecs)
+            if (lanes_pref * v >= dim && k1_shape_supported(lanes_pref, v)) return {lanes_pref, v};
+        return {};
+    }
+    for (const Shape& s : table)
+        if (s.lanes * s.vec >= dim) return s;
+    return {};
+}
+
+int row_stride_for(int dim, int lanes_pref) {
+    Shape s = choose_shape(dim, lanes_pref);
+    if (s.lanes > 0) return s.lanes * s.vec;
+    return (dim + 3) & ~3;
+}
+
+int context_width(const fw2v_config& c) { return (c.window + 1) / 2; }  // config.hpp:32
+
+void validate(const fw2v_config& c) {  // validate_config (config.cpp:165-177)
+    if (c.dim < 1) fail(FW2V_ERR_BAD_CONFIG, "dim must be >= 1");
+    if (c.window < 1) fail(FW2V_ERR_BAD_CONFIG, "window must be >= 1");
+    if (c.negatives < 0) fail(FW2V_ERR_BAD_CONFIG, "negatives must be >= 0");
+    if (c.epochs < 0) fail(FW2V_ERR_BAD_CONFIG, "epochs must be >= 0");
+    if (!(c.alpha0 > 0.0f)) fail(FW2V_ERR_BAD_CONFIG, "alpha must be > 0");
+    if (c.min_count < 1) fail(FW2V_ERR_BAD_CONFIG, "min_count must be >= 1");
+    if (c.batch_sentences < 1) fail(FW2V_ERR_BAD_CONFIG, "batch_sentences must be >= 1");
+    if (c.max_sentence_len < 1) fail(FW2V_ERR_BAD_CONFIG, "max_sentence_len must be >= 1");
+    if (c.workers < 0) fail(FW2V_ERR_BAD_CONFIG, "workers must be >= 0");
+    if (c.table_size < 1) fail(FW2V_ERR_BAD_CONFIG, "table_size must be >= 1");
+    if (!(c.table_power >= 0.0)) fail(FW2V_ERR_BAD_CONFIG, "table_power must be >= 0");
+    if (c.reuse_mode < 0 || c.reuse_mode > 3) fail(FW2V_ERR_BAD_CONFIG, "unknown reuse mode");
+    if (c.sampler < 0 || c.sampler > 1) fail(FW2V_ERR_BAD_CONFIG, "unknown sampler");
+}
+
+void require_device(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        fail(FW2V_ERR_NO_DEVICE, std::string("no CUDA device (the B200 trainer has no CPU path): ") +
+                                     (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+    if (device < 0 || device >= n) fail(FW2V_ERR_BAD_ARGUMENT, "device ordinal out of range");
+    FW2V_CK(cudaSetDevice(device));
+}
+
+// One producer lane: stream + two double-buffered batch slots.
+struct Slot {
+    int32_t* h_ids = nullptr;
+    uint32_t* h_off = nullptr;
+    int32_t* h_negs = nullptr;
+    float* h_alpha = nullptr;
+    int32_t* d_ids = nullptr;
+    uint32_t* d_off = nullptr;
+    int32_t* d_negs = nullptr;
+    float* d_alpha = nullptr;
+    cudaEvent_t h2d_done = nullptr;
+    bool in_flight = false;
+};
+
+struct Lane {
+    cudaStream_t stream = nullptr;
+    DevCounters* d_ctr = nullptr;
+    Slot slot[2];
+    uint64_t cap_words = 0, cap_sent = 0;
+    void release() {
+        for (Slot& s : slot) {
+            if (s.h2d_done) cudaEventSynchronize(s.h2d_done);
+            cudaFreeHost(s.h_ids); cudaFreeHost(s.h_off); cudaFreeHost(s.h_negs); cudaFreeHost(s.h_alpha);
+            cudaFree(s.d_ids); cudaFree(s.d_off); cudaFree(s.d_negs); cudaFree(s.d_alpha);
+            if (s.h2d_done) cudaEventDestroy(s.h2d_done);
+            s = Slot{};
+        }
+        cap_words = cap_sent = 0;
+    }
+};
+
+} // namespace
+
+struct fw2v_ctx {
+    fw2v_config cfg{};
+    int wf = 0;
+    int32_t vocab = 0;
+    Shape shape;
+    int stride = 0;
+    bool deterministic = false;
+    std::vector<uint64_t> counts;
+    uint64_t total_retained = 0;
+    std::vector<double> keep;
+    bool keep_on = false;
+    std::vector<int32_t> slots;
+    AliasTable alias;
+    float* syn0 = nullptr;
+    float* syn1 = nullptr;
+    bool own_model = true;
+    std::vector<Lane> lanes;
+    uint64_t words_trained = 0;  // schedule counter across calls (EmbeddingModel::words_trained)
+
+    ModelView model_view() const { return ModelView{syn0, syn1, cfg.dim, stride, vocab}; }
+
+    Sampler sampler() const {
+        Sampler s;
+        s.keep = keep_on ? keep.data() : nullptr;
+        s.n_neg = cfg.negatives;
+        if (cfg.sampler == FW2V_SAMPLER_ALIAS && !deterministic) {
+            s.alias = &alias;
+        } else {
+            s.slots = slots.data();
+            s.table_size = slots.size();
+        }
+        return s;
+    }
+
+    int producers() const {
+        if (deterministic) return 1;
+        int p = cfg.streams > 0 ? cfg.streams : cfg.workers;
+        if (p <= 0) {
+            unsigned hw = std::thread::hardware_concurrency();
+            p = hw == 0 ? 1 : static_cast<int>(hw);
+        }
+        return p;
+    }
+
+    cudaError_t launch(const BatchView& bv, bool serial, DevCounters* ctr, cudaStream_t st) const {
+        const ModelView mv = model_view();
+        if (serial) return launch_k2(mv, bv, cfg.negatives, wf, cfg.reuse_mode, true, ctr, st);
+        if (cfg.reuse_mode == kLifetime && shape.lanes > 0 && wf <= 5)
+            return launch_k1(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, cfg.fast_sigmoid != 0, ctr, st);
+        return launch_k2(mv, bv, cfg.negatives, wf, cfg.reuse_mode, false, ctr, st);
+    }
+
+    void ensure_lanes(int n, uint64_t cap_words, uint64_t cap_sent) {
+        FW2V_CK(cudaSetDevice(cfg.device));
+        if (static_cast<int>(lanes.size()) < n) lanes.resize(static_cast<size_t>(n));
+        const size_t nn = static_cast<size_t>(std::max(cfg.negatives, 1));
+        for (int i = 0; i < n; ++i) {
+            Lane& ln = lanes[static_cast<size_t>(i)];
+            if (!ln.stream) FW2V_CK(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+            if (!ln.d_ctr) FW2V_CK(cudaMalloc(&ln.d_ctr, sizeof(DevCounters)));
+            if (ln.cap_words >= cap_words && ln.cap_sent >= cap_sent) continue;
+            ln.release();
+            for (Slot& s : ln.slot) {
+                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_ids), 4 * cap_words, cudaHostAllocDefault));
+                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_negs), 4 * cap_words * nn, cudaHostAllocDefault));
+                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_off), 4 * (cap_sent + 1), cudaHostAllocDefault));
+                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_alpha), 4 * cap_sent, cudaHostAllocDefault));
+                FW2V_CK(cudaMalloc(&s.d_ids, 4 * cap_words));
+                FW2V_CK(cudaMalloc(&s.d_negs, 4 * cap_words * nn));
+                FW2V_CK(cudaMalloc(&s.d_off, 4 * (cap_sent + 1)));
+                FW2V_CK(cudaMalloc(&s.d_alpha, 4 * cap_sent));
+                FW2V_CK(cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming));
+            }
+            ln.cap_words = cap_words;
+            ln.cap_sent = cap_sent;
+        }
+    }
+
+    ~fw2v_ctx() {
+        cudaSetDevice(cfg.device);
+        for (Lane& ln : lanes) {
+            if (ln.stream) cudaStreamSynchronize(ln.stream);
+            ln.release();
+            cudaFree(ln.d_ctr);
+            if (ln.stream) cudaStreamDestroy(ln.stream);
+        }
+        if (own_model) {
+            cudaFree(syn0);
+            cudaFree(syn1);
+        }
+    }
+};
+
+struct fw2v_plan {
+    struct Batch {
+        BatchView view;
+    };
+    std::vector<std::vector<Batch>> lanes;
+    void* d_mem = nullptr;
+    size_t bytes = 0;
+    uint64_t words = 0, sentences = 0, batches = 0;
+    int device = 0;
+    ~fw2v_plan() {
+        if (d_mem) {
+            cudaSetDevice(device);
+            cudaFree(d_mem);
+        }
+    }
+};
+
+namespace {
+
+// Per-producer capacity: the largest batch a producer can assemble.
+void capacity_for(const CorpusView& c, uint64_t begin, uint64_t end, uint64_t S, uint64_t* words,
+                  uint64_t* sents) {
+    uint64_t maxlen = 0;
+    for (uint64_t s = begin; s < end; ++s) maxlen = std::max(maxlen, c.offsets[s + 1] - c.offsets[s]);
+    const uint64_t chunk_words = c.offsets[end] - c.offsets[begin];
+    *words = std::max<uint64_t>(1, std::min(chunk_words, S * maxlen));
+    *sents = std::max<uint64_t>(1, std::min(end - begin, S));
+}
+
+uint64_t expected_epoch_words(const fw2v_ctx& x) {  // trainer.cpp:378-386
+    if (!x.keep_on) return x.total_retained;
+    double e = 0.0;
+    for (int32_t w = 0; w < x.vocab; ++w) e += static_cast<double>(x.counts[static_cast<size_t>(w)]) * x.keep[static_cast<size_t>(w)];
+    const uint64_t r = static_cast<uint64_t>(e + 0.5);
+    return r > 0 ? r : 1;
+}
+
+} // namespace
+
+extern "C" {
+
+int fw2v_abi_version(void) { return FW2V_ABI_VERSION; }
+
+const char* fw2v_last_error(void) { return g_error.c_str(); }
+
+void fw2v_config_default(fw2v_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->dim = 128;
+    c->window = 5;
+    c->negatives = 5;
+    c->epochs = 20;
+    c->alpha0 = 0.025f;
+    c->subsample = 1e-4;
+    c->min_count = 5;
+    c->batch_sentences = 10000;
+    c->max_sentence_len = 1000;
+    c->workers = 0;
+    c->seed = 1;
+    c->reuse_mode = FW2V_REUSE_LIFETIME;
+    c->table_power = 0.75;
+    c->table_size = 10000000;
+    c->queue_capacity = 0;
+    c->ignore_delimiters = 1;
+    c->device = 0;
+    c->deterministic = -1;
+    c->sampler = FW2V_SAMPLER_REFERENCE;
+    c->fast_sigmoid = 1;
+    c->k1_lanes = 0;
+    c->streams = 0;
+}
+
+int fw2v_validate_config(const fw2v_config* cfg) {
+    return guarded([&] { validate(*cfg); });
+}
+
+int fw2v_device_count(int* count) {
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        g_error = cudaGetErrorString(e);
+        return FW2V_ERR_NO_DEVICE;
+    }
+    return FW2V_OK;
+}
+
+int32_t fw2v_row_stride(const fw2v_config* cfg) { return row_stride_for(cfg->dim, cfg->k1_lanes); }
+
+int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_size, fw2v_ctx** out) {
+    *out = nullptr;
+    return guarded([&] {
+        validate(*cfg);
+        if (vocab_size < 1) fail(FW2V_ERR_EMPTY_VOCAB, "corpus has an empty vocabulary");
+        auto x = std::make_unique<fw2v_ctx>();
+        x->cfg = *cfg;
+        if (x->cfg.workers == 0) {
+            unsigned hw = std::thread::hardware_concurrency();
+            x->cfg.workers = hw == 0 ? 1 : static_cast<int>(hw);  // resolve_config (config.cpp:190)
+        }
+        x->wf = context_width(x->cfg);
+        x->vocab = vocab_size;
+        x->deterministic = cfg->deterministic == 1 || (cfg->deterministic < 0 && x->cfg.workers == 1);
+        x->shape = choose_shape(cfg->dim, cfg->k1_lanes);
+        x->stride = row_stride_for(cfg->dim, cfg->k1_lanes);
+        if (!x->deterministic && cfg->reuse_mode == kLifetime && (x->shape.lanes == 0 || x->wf > 5))
+            fail(FW2V_ERR_UNSUPPORTED, "K1 covers dim <= 512 and window <= 10 (W_f <= 5)");
+        if (x->wf > 16) fail(FW2V_ERR_UNSUPPORTED, "window > 32 is not supported");
+        x->counts.assign(counts, counts + vocab_size);
+        for (uint64_t c : x->counts) x->total_retained += c;
+        x->keep.resize(static_cast<size_t>(vocab_size));
+        x->keep_on = keep_probs(counts, vocab_size, cfg->subsample, x->keep.data());
+        x->slots.resize(cfg->table_size);
+        build_table(counts, vocab_size, cfg->table_power, cfg->table_size, x->slots.data());
+        if (cfg->sampler == FW2V_SAMPLER_ALIAS) x->alias.build(counts, vocab_size, cfg->table_power);
+        require_device(cfg->device);
+        const size_t bytes = sizeof(float) * static_cast<size_t>(vocab_size) * static_cast<size_t>(x->stride);
+        FW2V_CK(cudaMalloc(&x->syn0, bytes));
+        FW2V_CK(cudaMalloc(&x->syn1, bytes));
+        Rng r = Rng::derive(cfg->seed, 0x696e6974ULL);  // "init" stream, model.cpp:26
+        FW2V_CK(launch_init_model(x->model_view(), r.state, nullptr));
+        FW2V_CK(cudaDeviceSynchronize());
+        *out = x.release();
+    });
+}
+
+void fw2v_destroy(fw2v_ctx* ctx) { delete ctx; }
+
+int fw2v_init_model(fw2v_ctx* x, uint64_t seed) {
+    return guarded([&] {
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        Rng r = Rng::derive(seed, 0x696e6974ULL);
+        FW2V_CK(launch_init_model(x->model_view(), r.state, nullptr));
+        FW2V_CK(cudaDeviceSynchronize());
+        x->words_trained = 0;
+    });
+}
+
+int fw2v_get_model(fw2v_ctx* x, float* input, float* output) {
+    return guarded([&] {
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        const size_t w = sizeof(float) * static_cast<size_t>(x->cfg.dim);
+        const size_t p = sizeof(float) * static_cast<size_t>(x->stride);
+        if (input) FW2V_CK(cudaMemcpy2D(input, w, x->syn0, p, w, static_cast<size_t>(x->vocab), cudaMemcpyDeviceToHost));
+        if (output) FW2V_CK(cudaMemcpy2D(output, w, x->syn1, p, w, static_cast<size_t>(x->vocab), cudaMemcpyDeviceToHost));
+    });
+}
+
+int fw2v_set_model(fw2v_ctx* x, const float* input, const float* output) {
+    return guarded([&] {
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        const size_t w = sizeof(float) * static_cast<size_t>(x->cfg.dim);
+        const size_t p = sizeof(float) * static_cast<size_t>(x->stride);
+        const size_t bytes = p * static_cast<size_t>(x->vocab);
+        if (input) {
+            FW2V_CK(cudaMemset(x->syn0, 0, bytes));
+            FW2V_CK(cudaMemcpy2D(x->syn0, p, input, w, w, static_cast<size_t>(x->vocab), cudaMemcpyHostToDevice));
+        }
+        if (output) {
+            FW2V_CK(cudaMemset(x->syn1, 0, bytes));
+            FW2V_CK(cudaMemcpy2D(x->syn1, p, output, w, w, static_cast<size_t>(x->vocab), cudaMemcpyHostToDevice));
+        }
+    });
+}
+
+int fw2v_model_device(fw2v_ctx* x, float** syn0, float** syn1, int32_t* stride) {
+    *syn0 = x->syn0;
+    *syn1 = x->syn1;
+    *stride = x->stride;
+    return FW2V_OK;
+}
+
+int fw2v_attach_model(fw2v_ctx* x, float* syn0, float* syn1) {
+    return guarded([&] {
+        if (!syn0 || !syn1) fail(FW2V_ERR_BAD_ARGUMENT, "null model pointer");
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        FW2V_CK(cudaDeviceSynchronize());
+        if (x->own_model) {
+            cudaFree(x->syn0);
+            cudaFree(x->syn1);
+        }
+        x->syn0 = syn0;
+        x->syn1 = syn1;
+        x->own_model = false;
+    });
+}
+
+int fw2v_train_sentences(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids,
+                         const int32_t* negatives, const float* alphas, int32_t serial,
+                         fw2v_counters* counters) {
+    return guarded([&] {
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        const uint64_t words = offsets[n_sentences] - offsets[0];
+        const int n = x->cfg.negatives;
+        std::vector<uint32_t> off(n_sentences + 1);
+        for (uint64_t s = 0; s <= n_sentences; ++s) off[s] = static_cast<uint32_t>(offsets[s] - offsets[0]);
+        int32_t *d_ids = nullptr, *d_negs = nullptr;
+        uint32_t* d_off = nullptr;
+        float* d_alpha = nullptr;
+        DevCounters* d_ctr = nullptr;
+        struct Free {
+            void* p[5];
+            ~Free() { for (void* q : p) cudaFree(q); }
+        } guard{{nullptr, nullptr, nullptr, nullptr, nullptr}};
+        FW2V_CK(cudaMalloc(&d_ids, 4 * std::max<uint64_t>(words, 1))); guard.p[0] = d_ids;
+        FW2V_CK(cudaMalloc(&d_negs, 4 * std::max<uint64_t>(words * n, 1))); guard.p[1] = d_negs;
+        FW2V_CK(cudaMalloc(&d_off, 4 * (n_sentences + 1))); guard.p[2] = d_off;
+        FW2V_CK(cudaMalloc(&d_alpha, 4 * std::max<uint64_t>(n_sentences, 1))); guard.p[3] = d_alpha;
+        FW2V_CK(cudaMalloc(&d_ctr, sizeof(DevCounters))); guard.p[4] = d_ctr;
+        FW2V_CK(cudaMemset(d_ctr, 0, sizeof(DevCounters)));
+        if (words) FW2V_CK(cudaMemcpy(d_ids, ids + offsets[0], 4 * words, cudaMemcpyHostToDevice));
+        if (words * n) FW2V_CK(cudaMemcpy(d_negs, negatives, 4 * words * n, cudaMemcpyHostToDevice));
+        FW2V_CK(cudaMemcpy(d_off, off.data(), 4 * (n_sentences + 1), cudaMemcpyHostToDevice));
+        if (n_sentences) FW2V_CK(cudaMemcpy(d_alpha, alphas, 4 * n_sentences, cudaMemcpyHostToDevice));
+        BatchView bv{d_ids, d_off, d_negs, d_alpha, static_cast<int32_t>(n_sentences)};
+        FW2V_CK(x->launch(bv, serial != 0, d_ctr, nullptr));
+        FW2V_CK(cudaDeviceSynchronize());
+        DevCounters h{};
+        FW2V_CK(cudaMemcpy(&h, d_ctr, sizeof(h), cudaMemcpyDeviceToHost));
+        if (counters) {
+            counters->context_reads = h.context_reads;
+            counters->context_writes = h.context_writes;
+            counters->sample_reads = h.sample_reads;
+            counters->sample_writes = h.sample_writes;
+            counters->ring_hits = h.ring_hits;
+            counters->words = h.words;
+            counters->sentences = h.sentences;
+        }
+    });
+}
+
+int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids,
+                      fw2v_observer_fn observer, void* observer_user, fw2v_epoch_fn on_epoch,
+                      void* epoch_user, fw2v_report* report) {
+    return guarded([&] {
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        const fw2v_config& cfg = x->cfg;
+        const CorpusView corpus{offsets, ids, n_sentences};
+        const int P = x->producers();
+        const uint64_t chunk = (n_sentences + P - 1) / std::max(P, 1);  // trainer.cpp:431-434
+        uint64_t cap_w = 1, cap_s = 1;
+        for (int p = 0; p < P; ++p) {
+            const uint64_t b = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
+            const uint64_t e = std::min(n_sentences, b + chunk);
+            uint64_t w, s;
+            capacity_for(corpus, b, e, cfg.batch_sentences, &w, &s);
+            cap_w = std::max(cap_w, w);
+            cap_s = std::max(cap_s, s);
+        }
+        x->ensure_lanes(P, cap_w, cap_s);
+        const uint64_t schedule_total =
+            cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
+        const Sampler sp = x->sampler();
+        const int n_neg = cfg.negatives;
+
+        fw2v_report rep{};
+        rep.vocab_size = static_cast<uint64_t>(x->vocab);
+        std::atomic<uint64_t> serial_ctr{0};
+        std::atomic<uint64_t> batch_words{0};
+        std::atomic<uint64_t> batch_nanos{0};
+        std::atomic<uint64_t> h2d{0};
+        std::mutex obs_mutex;
+        const double run_start = wall_seconds();
+
+        for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
+            for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), x->lanes[static_cast<size_t>(p)].stream));
+            std::atomic<uint64_t> reserved{x->words_trained};
+            std::vector<uint64_t> an_acc(static_cast<size_t>(P) * 5, 0);
+            std::vector<std::string> errors(static_cast<size_t>(P));
+            const double t0 = wall_seconds();
+            std::vector<std::thread> threads;
+            for (int p = 0; p < P; ++p) {
+                threads.emplace_back([&, p] {
+                    try {
+                        FW2V_CK(cudaSetDevice(cfg.device));
+                        Lane& ln = x->lanes[static_cast<size_t>(p)];
+                        const uint64_t begin = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
+                        const uint64_t end = std::min(n_sentences, begin + chunk);
+                        uint64_t cursor = begin;
+                        double cpu = 0.0;
+                        uint64_t wsum = 0;
+                        uint64_t* an = &an_acc[static_cast<size_t>(p) * 5];
+                        int which = 0;
+                        for (uint64_t k = 0; cursor < end; ++k) {
+                            Slot& sl = ln.slot[which];
+                            if (sl.in_flight) FW2V_CK(cudaEventSynchronize(sl.h2d_done));
+                            Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), k);
+                            const double c0 = thread_cpu_seconds();
+                            uint64_t words = 0;
+                            const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
+                            const uint64_t kept = assemble(corpus, cursor, end, cfg.batch_sentences, sp, rng, bo, &words);
+                            // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
+                            const uint64_t base = reserved.fetch_add(words);
+                            for (uint64_t q = 0; q < kept; ++q) sl.h_alpha[q] = lr_at(base + sl.h_off[q], schedule_total, cfg.alpha0);
+                            cpu += thread_cpu_seconds() - c0;
+                            wsum += words;
+                            if (kept == 0) continue;
+                            for (uint64_t q = 0; q < kept; ++q) {
+                                uint64_t t[5];
+                                analytic(sl.h_off[q + 1] - sl.h_off[q], x->wf, n_neg, cfg.reuse_mode, t);
+                                for (int z = 0; z < 5; ++z) an[z] += t[z];
+                            }
+                            if (observer) {
+                                const uint64_t s0 = serial_ctr.fetch_add(kept);
+                                std::lock_guard<std::mutex> lk(obs_mutex);
+                                for (uint64_t q = 0; q < kept; ++q)
+                                    for (uint32_t i = 0; i < sl.h_off[q + 1] - sl.h_off[q]; ++i) observer(observer_user, s0 + q, i);
+                            }
+                            cudaStream_t st = ln.stream;
+                            FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, st));
+                            if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, st));
+                            FW2V_CK(cudaMemcpyAsync(sl.d_off, sl.h_off, 4 * (kept + 1), cudaMemcpyHostToDevice, st));
+                            FW2V_CK(cudaMemcpyAsync(sl.d_alpha, sl.h_alpha, 4 * kept, cudaMemcpyHostToDevice, st));
+                            FW2V_CK(cudaEventRecord(sl.h2d_done, st));
+                            sl.in_flight = true;
+                            h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
+                            const BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
+                            FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st));
+                            which ^= 1;
+                        }
+                        batch_words.fetch_add(wsum);
+                        batch_nanos.fetch_add(static_cast<uint64_t>(cpu * 1e9));
+                    } catch (const Failure& f) {
+                        errors[static_cast<size_t>(p)] = f.msg;
+                    }
+                });
+            }
+            for (auto& t : threads) t.join();
+            for (int p = 0; p < P; ++p) FW2V_CK(cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream));
+            for (const auto& e : errors)
+                if (!e.empty()) fail(FW2V_ERR_CUDA, e);
+            const double secs = wall_seconds() - t0;
+            uint64_t epoch_words = 0;
+            for (int p = 0; p < P; ++p) {
+                DevCounters h{};
+                FW2V_CK(cudaMemcpy(&h, x->lanes[static_cast<size_t>(p)].d_ctr, sizeof(h), cudaMemcpyDeviceToHost));
+                rep.traffic.context_reads += h.context_reads;
+                rep.traffic.context_writes += h.context_writes;
+                rep.traffic.sample_reads += h.sample_reads;
+                rep.traffic.sample_writes += h.sample_writes;
+                rep.traffic.ring_hits += h.ring_hits;
+                rep.traffic.words += h.words;
+                rep.traffic.sentences += h.sentences;
+                epoch_words += h.words;
+                rep.sentences_trained += h.sentences;
+                const uint64_t* an = &an_acc[static_cast<size_t>(p) * 5];
+                rep.analytic.context_reads += an[0];
+                rep.analytic.context_writes += an[1];
+                rep.analytic.sample_reads += an[2];
+                rep.analytic.sample_writes += an[3];
+                rep.analytic.ring_hits += an[4];
+            }
+            x->words_trained += epoch_words;
+            rep.words_trained += epoch_words;
+            rep.n_epochs = epoch + 1;
+            if (on_epoch) {
+                fw2v_epoch_stats st{epoch, epoch_words, secs, secs > 0 ? static_cast<double>(epoch_words) / secs : 0.0};
+                on_epoch(epoch_user, &st);
+            }
+        }
+        rep.analytic.words = rep.traffic.words;
+        rep.analytic.sentences = rep.traffic.sentences;
+        rep.wall_seconds = wall_seconds() - run_start;
+        const uint64_t ns = batch_nanos.load();
+        rep.batching_words_per_sec = ns > 0 ? static_cast<double>(batch_words.load()) * 1e9 / static_cast<double>(ns) : 0.0;
+        rep.h2d_bytes = h2d.load();
+        if (report) *report = rep;
+    });
+}
+
+int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids,
+                    int32_t epoch, fw2v_plan** out) {
+    *out = nullptr;
+    return guarded([&] {
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        const fw2v_config& cfg = x->cfg;
+        const CorpusView corpus{offsets, ids, n_sentences};
+        const int P = x->producers();
+        const uint64_t chunk = (n_sentences + P - 1) / std::max(P, 1);
+        const uint64_t schedule_total =
+            cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
+        const Sampler sp = x->sampler();
+        const int n_neg = cfg.negatives;
+        struct HostBatch {
+            std::vector<int32_t> ids, negs;
+            std::vector<uint32_t> off;
+            std::vector<float> alpha;
+        };
+        std::vector<std::vector<HostBatch>> host(static_cast<size_t>(P));
+        std::atomic<uint64_t> reserved{x->words_trained};
+        std::vector<std::thread> threads;
+        for (int p = 0; p < P; ++p) {
+            threads.emplace_back([&, p] {
+                const uint64_t begin = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
+                const uint64_t end = std::min(n_sentences, begin + chunk);
+                uint64_t cap_w, cap_s;
+                capacity_for(corpus, begin, std::max(begin, end), cfg.batch_sentences, &cap_w, &cap_s);
+                std::vector<int32_t> bi(cap_w), bn(cap_w * std::max(n_neg, 1));
+                std::vector<uint32_t> bo(cap_s + 1);
+                uint64_t cursor = begin;
+                for (uint64_t k = 0; cursor < end; ++k) {
+                    Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), k);
+                    uint64_t words = 0;
+                    const uint64_t kept = assemble(corpus, cursor, end, cfg.batch_sentences, sp, rng,
+                                                   BatchOut{bi.data(), bo.data(), bn.data(), cap_w, cap_s}, &words);
+                    if (kept == 0) continue;
+                    HostBatch hb;
+                    hb.ids.assign(bi.begin(), bi.begin() + static_cast<ptrdiff_t>(words));
+                    hb.negs.assign(bn.begin(), bn.begin() + static_cast<ptrdiff_t>(words * n_neg));
+                    hb.off.assign(bo.begin(), bo.begin() + static_cast<ptrdiff_t>(kept + 1));
+                    const uint64_t base = reserved.fetch_add(words);
+                    hb.alpha.resize(kept);
+                    for (uint64_t q = 0; q < kept; ++q) hb.alpha[q] = lr_at(base + bo[q], schedule_total, cfg.alpha0);
+                    host[static_cast<size_t>(p)].push_back(std::move(hb));
+                }
+            });
+        }
+        for (auto& t : threads) t.join();
+        auto plan = std::make_unique<fw2v_plan>();
+        plan->device = cfg.device;
+        auto a16 = [](size_t b) { return (b + 255) & ~size_t(255); };
+        size_t bytes = 0;
+        for (auto& lane : host)
+            for (auto& hb : lane)
+                bytes += a16(4 * hb.ids.size()) + a16(4 * std::max<size_t>(hb.negs.size(), 1)) + a16(4 * hb.off.size()) + a16(4 * hb.alpha.size());
+        FW2V_CK(cudaMalloc(&plan->d_mem, std::max<size_t>(bytes, 256)));
+        plan->bytes = bytes;
+        char* base = static_cast<char*>(plan->d_mem);
+        plan->lanes.resize(static_cast<size_t>(P));
+        for (int p = 0; p < P; ++p) {
+            for (auto& hb : host[static_cast<size_t>(p)]) {
+                auto put = [&](const void* src, size_t n) {
+                    char* dst = base;
+                    if (n) FW2V_CK(cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice));
+                    base += a16(std::max<size_t>(n, 1));
+                    return dst;
+                };
+                fw2v_plan::Batch b;
+                b.view.ids = reinterpret_cast<const int32_t*>(put(hb.ids.data(), 4 * hb.ids.size()));
+                b.view.negs = reinterpret_cast<const int32_t*>(put(hb.negs.data(), 4 * hb.negs.size()));
+                b.view.offsets = reinterpret_cast<const uint32_t*>(put(hb.off.data(), 4 * hb.off.size()));
+                b.view.alpha = reinterpret_cast<const float*>(put(hb.alpha.data(), 4 * hb.alpha.size()));
+                b.view.n_sentences = static_cast<int32_t>(hb.alpha.size());
+                plan->lanes[static_cast<size_t>(p)].push_back(b);
+                plan->words += hb.ids.size();
+                plan->sentences += hb.alpha.size();
+                plan->batches += 1;
+            }
+            host[static_cast<size_t>(p)].clear();
+        }
+        *out = plan.release();
+    });
+}
+
+int fw2v_plan_info(const fw2v_plan* plan, uint64_t* words, uint64_t* sentences, uint64_t* batches,
+                   uint64_t* device_bytes) {
+    if (words) *words = plan->words;
+    if (sentences) *sentences = plan->sentences;
+    if (batches) *batches = plan->batches;
+    if (device_bytes) *device_bytes = plan->bytes;
+    return FW2V_OK;
+}
+
+int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* counters) {
+    return guarded([&] {
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        const int P = static_cast<int>(plan->lanes.size());
+        x->ensure_lanes(P, 1, 1);
+        cudaEvent_t start, fork;
+        std::vector<cudaEvent_t> ends(static_cast<size_t>(P));
+        FW2V_CK(cudaEventCreate(&start));
+        FW2V_CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        for (auto& e : ends) FW2V_CK(cudaEventCreate(&e));
+        cudaStream_t s0 = x->lanes[0].stream;
+        for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), s0));
+        FW2V_CK(cudaEventRecord(start, s0));
+        FW2V_CK(cudaEventRecord(fork, s0));
+        for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, fork, 0));
+        // Interleave launches across lanes so each stream always has queued work.
+        size_t maxb = 0;
+        for (auto& l : plan->lanes) maxb = std::max(maxb, l.size());
+        for (size_t k = 0; k < maxb; ++k)
+            for (int p = 0; p < P; ++p)
+                if (k < plan->lanes[static_cast<size_t>(p)].size())
+                    FW2V_CK(x->launch(plan->lanes[static_cast<size_t>(p)][k].view, x->deterministic,
+                                      x->lanes[static_cast<size_t>(p)].d_ctr, x->lanes[static_cast<size_t>(p)].stream));
+        for (int p = 0; p < P; ++p) FW2V_CK(cudaEventRecord(ends[static_cast<size_t>(p)], x->lanes[static_cast<size_t>(p)].stream));
+        float ms_max = 0.0f;
+        for (int p = 0; p < P; ++p) {
+            FW2V_CK(cudaEventSynchronize(ends[static_cast<size_t>(p)]));
+            float ms = 0.0f;
+            FW2V_CK(cudaEventElapsedTime(&ms, start, ends[static_cast<size_t>(p)]));
+            ms_max = std::max(ms_max, ms);
+        }
+        if (seconds) *seconds = 1e-3 * ms_max;
+        fw2v_counters c{};
+        for (int p = 0; p < P; ++p) {
+            DevCounters h{};
+            FW2V_CK(cudaMemcpy(&h, x->lanes[static_cast<size_t>(p)].d_ctr, sizeof(h), cudaMemcpyDeviceToHost));
+            c.context_reads += h.context_reads;
+            c.context_writes += h.context_writes;
+            c.sample_reads += h.sample_reads;
+            c.sample_writes += h.sample_writes;
+            c.ring_hits += h.ring_hits;
+            c.words += h.words;
+            c.sentences += h.sentences;
+        }
+        if (counters) *counters = c;
+        x->words_trained += c.words;
+        cudaEventDestroy(start);
+        cudaEventDestroy(fork);
+        for (auto& e : ends) cudaEventDestroy(e);
+    });
+}
+
+void fw2v_plan_destroy(fw2v_plan* plan) { delete plan; }
+
+int fw2v_keep_probs(const uint64_t* counts, int32_t vocab_size, double threshold, double* out) {
+    return keep_probs(counts, vocab_size, threshold, out) ? 1 : 0;
+}
+
+int fw2v_table_build(const uint64_t* counts, int32_t vocab_size, double power, uint64_t size, int32_t* out_slots) {
+    return guarded([&] { build_table(counts, vocab_size, power, size, out_slots); });
+}
+
+int64_t fw2v_assemble_batch(const uint64_t* counts, int32_t vocab_size, const uint64_t* offsets,
+                            uint64_t n_sentences, const int32_t* ids, uint64_t* cursor, uint64_t max_sentences,
+                            int32_t negatives, double power, uint64_t table_size, double threshold,
+                            uint64_t seed, uint64_t a, uint64_t b, uint64_t c, int32_t* out_ids,
+                            uint64_t* out_offsets, int32_t* out_negs) {
+    int64_t kept = 0;
+    int rc = guarded([&] {
+        if (max_sentences < 1) fail(FW2V_ERR_BAD_ARGUMENT, "batch size must be >= 1");
+        if (negatives < 0) fail(FW2V_ERR_BAD_ARGUMENT, "negatives must be >= 0");
+        std::vector<int32_t> slots(table_size);
+        build_table(counts, vocab_size, power, table_size, slots.data());
+        std::vector<double> keep(static_cast<size_t>(vocab_size));
+        const bool on = keep_probs(counts, vocab_size, threshold, keep.data());
+        Sampler sp;
+        sp.keep = on ? keep.data() : nullptr;
+        sp.slots = slots.data();
+        sp.table_size = table_size;
+        sp.n_neg = negatives;
+        const uint64_t total = offsets[n_sentences] - offsets[0];
+        std::vector<uint32_t> off(n_sentences + 1);
+        Rng rng = Rng::derive(seed, a, b, c);
+        uint64_t words = 0;
+        uint64_t cur = *cursor;
+        kept = static_cast<int64_t>(assemble(CorpusView{offsets, ids, n_sentences}, cur, n_sentences, max_sentences, sp, rng,
+                                             BatchOut{out_ids, off.data(), out_negs, total + 1, n_sentences + 1}, &words));
+        *cursor = cur;
+        for (int64_t q = 0; q <= kept; ++q) out_offsets[q] = off[static_cast<size_t>(q)];
+    });
+    return rc == FW2V_OK ? kept : -rc;
+}
+
+float fw2v_lr_at(uint64_t words_trained, uint64_t total, float alpha0) {
+    if (total == 0) {
+        g_error = "total_words must be > 0";
+        return -1.0f;
+    }
+    return lr_at(words_trained, total, alpha0);
+}
+
+int fw2v_analytic_traffic(uint64_t length, int32_t width, int32_t negatives, int32_t mode, fw2v_counters* out) {
+    return guarded([&] {
+        if (length < 1) fail(FW2V_ERR_BAD_ARGUMENT, "sentence length must be >= 1");
+        if (width < 1) fail(FW2V_ERR_BAD_ARGUMENT, "context width must be >= 1");
+        if (negatives < 0) fail(FW2V_ERR_BAD_ARGUMENT, "negatives must be >= 0");
+        uint64_t t[5];
+        analytic(length, width, negatives, mode, t);
+        *out = fw2v_counters{t[0], t[1], t[2], t[3], t[4], length, 1};
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,631 @@
+// FULL-W2V SGNS training kernels for B200 (sm_100a).
+//
+// K1  k1_lifetime   — the performance path (Hogwild across sentences). One
+//                     lane group (LANES lanes, LANES | 32) owns one sentence;
+//                     each lane owns VEC contiguous columns of every row. The
+//                     2*W_f+1 ring of syn0 rows (reference ContextRing,
+//                     trainer.cpp:32-102) lives in registers for the sentence's
+//                     whole lifetime and slides by register renaming; each
+//                     sample row (target + N negatives, syn1) is register-
+//                     resident across its sweep over the 2*W_f context rows
+//                     (sweep_samples, trainer.cpp:133-154) and the next sweep's
+//                     row is prefetched while the current one runs. Dots are
+//                     LANES-wide xor-butterfly reductions; no tensor cores
+//                     (per-pair contractions are d-long and latency bound).
+//                     Per-sentence arithmetic order = reference order
+//                     (samples outer, contexts inner, incremental updates);
+//                     only the dot association and sigmoid differ.
+// K2  k2_exact      — the deterministic / exact engine: a warp restates the
+//                     reference FP contract bit for bit (4 strided partial sums,
+//                     no FMA, double-precision exp sigmoid; kernels.hpp:10-33,
+//                     model.cpp:34-37) and every reuse mode's access order
+//                     (trainer.cpp:237-328). serial=1 runs all sentences of a
+//                     batch in order on one warp (== reference workers=1).
+// Kinit             — init_model (model.cpp:15-32) as a counter-based kernel:
+//                     splitmix64 draw i is mix(state0 + (i+1)*golden).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fw2v_device.cuh"
+
+namespace fw2v {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kK1Threads = 128;
+
+// ------------------------------------------------------------------ row I/O
+// Model rows go through L2 only (ld.global.cg / st.global.cg): other SMs
+// update them concurrently (Hogwild), and L1 is not coherent within a launch.
+template <int VEC>
+struct Row {
+    __device__ __forceinline__ static void load(float (&v)[VEC], const float* p) {
+        if constexpr (VEC % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 4) {
+                float4 t = __ldcg(reinterpret_cast<const float4*>(p + i));
+                v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+            }
+        } else if constexpr (VEC % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 2) {
+                float2 t = __ldcg(reinterpret_cast<const float2*>(p + i));
+                v[i] = t.x; v[i + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) v[i] = __ldcg(p + i);
+        }
+    }
+    __device__ __forceinline__ static void store(float* p, const float (&v)[VEC]) {
+        if constexpr (VEC % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 4)
+                __stcg(reinterpret_cast<float4*>(p + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        } else if constexpr (VEC % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 2)
+                __stcg(reinterpret_cast<float2*>(p + i), make_float2(v[i], v[i + 1]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) __stcg(p + i, v[i]);
+        }
+    }
+};
+
+template <int VEC>
+__device__ __forceinline__ void vzero(float (&v)[VEC]) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = 0.0f;
+}
+
+template <int VEC>
+__device__ __forceinline__ void vcopy(float (&d)[VEC], const float (&s)[VEC]) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) d[i] = s[i];
+}
+
+template <int LANES>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+    for (int o = LANES / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// g = (label - sigma(clamp(f, -6, 6))) * alpha   (trainer.cpp:147, model.cpp:34-37)
+template <bool FAST>
+__device__ __forceinline__ float sgd_coeff(float f, float label, float alpha) {
+    f = fminf(fmaxf(f, -6.0f), 6.0f);
+    float sig;
+    if constexpr (FAST) {
+        sig = fmaf(0.5f, tanh_approx(0.5f * f), 0.5f);  // |err| < 1e-3 (SPEC fast-sigmoid bound)
+    } else {
+        sig = 1.0f / (1.0f + expf(-f));
+    }
+    return (label - sig) * alpha;
+}
+
+// ---------------------------------------------------------------- K1 kernel
+template <int LANES, int VEC, int WF, bool FAST>
+__global__ void __launch_bounds__(kK1Threads)
+k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) {
+    constexpr int NCTX = 2 * WF;
+    constexpr int GPW = 32 / LANES;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & (LANES - 1);
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int sent = warp * GPW + lane / LANES;
+    const bool has = sent < b.n_sentences;
+
+    uint32_t beg = 0, len = 0;
+    float alpha = 0.0f;
+    if (has) {
+        beg = __ldg(b.offsets + sent);
+        len = __ldg(b.offsets + sent + 1) - beg;
+        alpha = __ldg(b.alpha + sent);
+    }
+    const int L = static_cast<int>(len);
+    const int Lmax = static_cast<int>(__reduce_max_sync(kFull, len));
+    if (Lmax == 0) return;  // warp-uniform
+
+    const int32_t* __restrict__ ids = b.ids + beg;
+    const int32_t* __restrict__ negs = b.negs + static_cast<size_t>(beg) * n_neg;
+    const size_t stride = static_cast<size_t>(m.stride);
+    float* __restrict__ syn0 = m.syn0 + sub * VEC;
+    float* __restrict__ syn1 = m.syn1 + sub * VEC;
+
+    // Window-relative ring: ctx[r] holds position i-WF+r (r < WF) or
+    // i+1+(r-WF) (r >= WF); tgt holds position i. tok = -1 outside [0, L).
+    float ctx[NCTX][VEC];
+    int tok[NCTX];
+    float tgt[VEC];
+    int ttok = L > 0 ? __ldg(ids) : -1;
+    if (ttok >= 0) Row<VEC>::load(tgt, syn0 + ttok * stride); else vzero(tgt);
+#pragma unroll
+    for (int r = 0; r < NCTX; ++r) {
+        const int p = r - WF + 1;
+        tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
+        if (tok[r] >= 0) Row<VEC>::load(ctx[r], syn0 + tok[r] * stride); else vzero(ctx[r]);
+    }
+    unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
+    unsigned c_writes = 0, s_rw = 0, pairs = 0;
+
+    // Sample pipeline: nxt holds the prefetched row of the upcoming sweep.
+    float s[VEC], nxt[VEC];
+    int nxt_sid = L >= 2 ? ttok : -1;
+    if (nxt_sid >= 0) Row<VEC>::load(nxt, syn1 + nxt_sid * stride); else vzero(nxt);
+    vzero(s);
+    int prev_sid = -1;
+
+    for (int i = 0; i < Lmax; ++i) {
+        const bool act = i < L;
+        const bool wact = act && L >= 2;
+        // Row entering the span for window i+1 (ContextRing::advance, trainer.cpp:55-69).
+        const int q = i + 1 + WF;
+        const int inc_tok = q < L ? __ldg(ids + q) : -1;
+        float inc[VEC];
+        if (inc_tok >= 0) Row<VEC>::load(inc, syn0 + inc_tok * stride); else vzero(inc);
+        c_reads += inc_tok >= 0;
+
+        for (int k = 0; k <= n_neg; ++k) {
+            const int sid = nxt_sid;
+            // The prefetch was issued before the previous sweep wrote its row
+            // back: forward the register copy when both sweeps hit one row.
+            if (sid != prev_sid) vcopy(s, nxt);
+            // Prefetch the next sweep's row: (i, k+1) or (i+1, 0).
+            {
+                const bool same_win = k < n_neg;
+                const int ni = same_win ? i : i + 1;
+                const bool nact = ni < L && L >= 2;
+                int ns = -1;
+                if (nact) ns = same_win ? __ldg(negs + static_cast<size_t>(i) * n_neg + k) : tok[WF];
+                nxt_sid = ns;
+                if (ns >= 0) Row<VEC>::load(nxt, syn1 + ns * stride);
+            }
+            const float label = k == 0 ? 1.0f : 0.0f;
+#pragma unroll
+            for (int r = 0; r < NCTX; ++r) {
+                float part = 0.0f;
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) part = fmaf(ctx[r][e], s[e], part);
+                const float f = group_sum<LANES>(part);
+                const bool valid = wact && tok[r] >= 0;
+                const float g = valid ? sgd_coeff<FAST>(f, label, alpha) : 0.0f;
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                    const float c = ctx[r][e];
+                    ctx[r][e] = fmaf(g, s[e], c);
+                    s[e] = fmaf(g, c, s[e]);
+                }
+                pairs += valid;
+            }
+            if (wact) Row<VEC>::store(syn1 + sid * stride, s);
+            s_rw += wact;
+            prev_sid = wact ? sid : -1;
+        }
+
+        // Slide: position i-WF leaves the span and is written back.
+        const int etok = tok[0];
+        if (etok >= 0) {
+            Row<VEC>::store(syn0 + etok * stride, ctx[0]);
+            ++c_writes;
+            if (inc_tok == etok) vcopy(inc, ctx[0]);  // load-after-evict forwarding
+        }
+#pragma unroll
+        for (int r = 0; r < WF - 1; ++r) { vcopy(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
+        vcopy(ctx[WF - 1], tgt);
+        tok[WF - 1] = act ? ttok : -1;
+        vcopy(tgt, ctx[WF]);
+        ttok = tok[WF];
+#pragma unroll
+        for (int r = WF; r < NCTX - 1; ++r) { vcopy(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
+        vcopy(ctx[NCTX - 1], inc);
+        tok[NCTX - 1] = inc_tok;
+    }
+    // ContextRing::finish (trainer.cpp:71-75): residents still in registers.
+#pragma unroll
+    for (int r = 0; r < NCTX; ++r) {
+        if (tok[r] >= 0) { Row<VEC>::store(syn0 + tok[r] * stride, ctx[r]); ++c_writes; }
+    }
+    if (ttok >= 0) { Row<VEC>::store(syn0 + ttok * stride, tgt); ++c_writes; }
+
+    if (ctr != nullptr) {
+        // One count per sentence: lane 0 of each group contributes.
+        const bool lead = has && sub == 0;
+        unsigned hits = (L >= 2) ? pairs - static_cast<unsigned>(L) : 0u;
+        unsigned v0 = __reduce_add_sync(kFull, lead ? c_reads : 0u);
+        unsigned v1 = __reduce_add_sync(kFull, lead ? c_writes : 0u);
+        unsigned v2 = __reduce_add_sync(kFull, lead ? s_rw : 0u);
+        unsigned v4 = __reduce_add_sync(kFull, lead ? hits : 0u);
+        unsigned v5 = __reduce_add_sync(kFull, lead ? static_cast<unsigned>(L) : 0u);
+        unsigned v6 = __reduce_add_sync(kFull, lead ? 1u : 0u);
+        if (lane == 0) {
+            atomicAdd(&ctr->context_reads, v0);
+            atomicAdd(&ctr->context_writes, v1);
+            atomicAdd(&ctr->sample_reads, v2);
+            atomicAdd(&ctr->sample_writes, v2);
+            atomicAdd(&ctr->ring_hits, v4);
+            atomicAdd(&ctr->words, v5);
+            atomicAdd(&ctr->sentences, v6);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K2 kernel
+// Bit-exact restatement of the reference arithmetic (default -O2 build: no
+// FMA; dot = 4 strided partial sums, kernels.hpp:10-22; update c+g*s and
+// s+g*c from pairing-entry values, kernels.hpp:26-33; sigmoid in double,
+// model.cpp:34-37).
+
+// Warp-cooperative dot in the reference association: lane m (< 4) runs
+// partial sum m sequentially; lane 0 folds (s0+s1)+(s2+s3) and the tail.
+__device__ __forceinline__ float dot_exact(const float* a, const float* b, int d, int lane) {
+    float sm = 0.0f;
+    const int d4 = d & ~3;
+    if (lane < 4) {
+        for (int k = lane; k < d4; k += 4) sm = __fadd_rn(sm, __fmul_rn(a[k], b[k]));
+    }
+    const float s1 = __shfl_down_sync(kFull, sm, 1);
+    const float s2 = __shfl_down_sync(kFull, sm, 2);
+    const float s3 = __shfl_down_sync(kFull, sm, 3);
+    float s = __fadd_rn(__fadd_rn(sm, s1), __fadd_rn(s2, s3));
+    if (lane == 0) {
+        for (int k = d4; k < d; ++k) s = __fadd_rn(s, __fmul_rn(a[k], b[k]));
+    }
+    return __shfl_sync(kFull, s, 0);
+}
+
+__device__ __forceinline__ float sigmoid_exact(float x) {
+    const float c = x < -6.0f ? -6.0f : (6.0f < x ? 6.0f : x);  // std::clamp
+    return static_cast<float>(1.0 / (1.0 + exp(-static_cast<double>(c))));
+}
+
+__device__ __forceinline__ float coeff_exact(float f, float label, float alpha) {
+    return __fmul_rn(__fsub_rn(label, sigmoid_exact(f)), alpha);
+}
+
+__device__ __forceinline__ void pair_update_exact(float* c, float* s, float g, int d, int lane) {
+    for (int k = lane; k < d; k += 32) {
+        const float cv = c[k], sv = s[k];
+        c[k] = __fadd_rn(cv, __fmul_rn(g, sv));
+        s[k] = __fadd_rn(sv, __fmul_rn(g, cv));
+    }
+}
+
+__device__ __forceinline__ void axpy_exact(float* y, const float* x, float g, int d, int lane) {
+    for (int k = lane; k < d; k += 32) y[k] = __fadd_rn(y[k], __fmul_rn(g, x[k]));
+}
+
+__device__ __forceinline__ void row_get(float* dst, const float* src, int d, int lane) {
+    for (int k = lane; k < d; k += 32) dst[k] = __ldcg(src + k);
+}
+__device__ __forceinline__ void row_put(float* dst, const float* src, int d, int lane) {
+    for (int k = lane; k < d; k += 32) __stcg(dst + k, src[k]);
+}
+
+constexpr int kMaxRing = 2 * 16 + 1;
+
+// smem layout (floats): ring[C*d] sample[d] a[(2WF)*d] b[(N+1)*d] c[(2WF)*d] e[(N+1)*d]
+__global__ void __launch_bounds__(32)
+k2_exact(ModelView m, BatchView b, int n_neg, int wf, int mode, int serial,
+         DevCounters* __restrict__ ctr) {
+    extern __shared__ float sh[];
+    __shared__ int slot_pos[kMaxRing];
+    __shared__ int slot_used[kMaxRing];
+    __shared__ int ctx_pos[2 * 16];
+    const int lane = threadIdx.x;
+    const int d = m.dim;
+    const int cap = 2 * wf + 1;
+    const size_t stride = static_cast<size_t>(m.stride);
+    float* ring = sh;
+    float* sample = ring + cap * d;
+    float* snap_ctx = sample + d;             // also window-mode local copies
+    float* snap_smp = snap_ctx + 2 * wf * d;
+    float* delta_ctx = snap_smp + (n_neg + 1) * d;
+    float* delta_smp = delta_ctx + 2 * wf * d;
+
+    unsigned long long cr = 0, cw = 0, sr = 0, sw = 0, hits = 0, words = 0, nsent = 0;
+
+    const int first = serial ? 0 : blockIdx.x;
+    const int last = serial ? b.n_sentences : min(b.n_sentences, static_cast<int>(blockIdx.x) + 1);
+    for (int sidx = first; sidx < last; ++sidx) {
+        const uint32_t beg = b.offsets[sidx];
+        const int L = static_cast<int>(b.offsets[sidx + 1] - beg);
+        const int32_t* ids = b.ids + beg;
+        const int32_t* negs = b.negs + static_cast<size_t>(beg) * n_neg;
+        const float alpha = b.alpha[sidx];
+        words += L;
+        nsent += 1;
+        auto in_row = [&](int pos) { return m.syn0 + ids[pos] * stride; };
+        auto out_row = [&](int id) { return m.syn1 + id * stride; };
+
+        if (mode == kLifetime || mode == kWindowSnapshot) {
+            // train_sentence_ring (trainer.cpp:237-255) with ContextRing.
+            if (lane < cap) { slot_pos[lane] = -1; slot_used[lane] = 0; }
+            __syncwarp();
+            int next_load = 0;
+            for (int i = 0; i < L; ++i) {
+                const int hi = min(L - 1, i + wf);  // advance (trainer.cpp:55-69)
+                while (next_load <= hi) {
+                    const int slot = next_load % cap;
+                    if (slot_pos[slot] >= 0) {
+                        row_put(in_row(slot_pos[slot]), ring + slot * d, d, lane);
+                        ++cw;
+                    }
+                    row_get(ring + slot * d, in_row(next_load), d, lane);
+                    ++cr;
+                    __syncwarp();
+                    if (lane == 0) { slot_pos[slot] = next_load; slot_used[slot] = 0; }
+                    __syncwarp();
+                    ++next_load;
+                }
+                const int lo = max(0, i - wf), hh = min(L - 1, i + wf);
+                int n_ctx = 0;
+                for (int j = lo; j <= hh; ++j)
+                    if (j != i) { if (lane == 0) ctx_pos[n_ctx] = j; ++n_ctx; }
+                __syncwarp();
+                if (n_ctx == 0) continue;
+                const int target = ids[i];
+                if (mode == kLifetime) {
+                    for (int k = 0; k <= n_neg; ++k) {  // sweep_samples (trainer.cpp:133-154)
+                        const int sid = k == 0 ? target : negs[static_cast<size_t>(i) * n_neg + k - 1];
+                        const float label = k == 0 ? 1.0f : 0.0f;
+                        row_get(sample, out_row(sid), d, lane);
+                        ++sr;
+                        __syncwarp();
+                        for (int j = 0; j < n_ctx; ++j) {
+                            const int slot = ctx_pos[j] % cap;
+                            if (slot_used[slot]) ++hits;
+                            __syncwarp();
+                            if (lane == 0) slot_used[slot] = 1;
+                            float* cv = ring + slot * d;
+                            const float f = dot_exact(cv, sample, d, lane);
+                            const float g = coeff_exact(f, label, alpha);
+                            pair_update_exact(cv, sample, g, d, lane);
+                            __syncwarp();
+                        }
+                        row_put(out_row(sid), sample, d, lane);
+                        ++sw;
+                        __syncwarp();
+                    }
+                } else {  // sweep_samples_snapshot (trainer.cpp:158-205)
+                    const int S = n_neg + 1;
+                    for (int j = 0; j < n_ctx; ++j)
+                        for (int e = lane; e < d; e += 32) snap_ctx[j * d + e] = ring[(ctx_pos[j] % cap) * d + e];
+                    for (int k = 0; k < S; ++k) {
+                        const int sid = k == 0 ? target : negs[static_cast<size_t>(i) * n_neg + k - 1];
+                        row_get(snap_smp + k * d, out_row(sid), d, lane);
+                        ++sr;
+                    }
+                    for (int e = lane; e < n_ctx * d; e += 32) delta_ctx[e] = 0.0f;
+                    for (int e = lane; e < S * d; e += 32) delta_smp[e] = 0.0f;
+                    __syncwarp();
+                    for (int k = 0; k < S; ++k) {
+                        const float label = k == 0 ? 1.0f : 0.0f;
+                        for (int j = 0; j < n_ctx; ++j) {
+                            const int slot = ctx_pos[j] % cap;
+                            if (slot_used[slot]) ++hits;
+                            __syncwarp();
+                            if (lane == 0) slot_used[slot] = 1;
+                            const float* cv = snap_ctx + j * d;
+                            const float* smp = snap_smp + k * d;
+                            const float f = dot_exact(cv, smp, d, lane);
+                            const float g = coeff_exact(f, label, alpha);
+                            axpy_exact(delta_ctx + j * d, smp, g, d, lane);
+                            axpy_exact(delta_smp + k * d, cv, g, d, lane);
+                            __syncwarp();
+                        }
+                    }
+                    for (int j = 0; j < n_ctx; ++j) {
+                        float* cv = ring + (ctx_pos[j] % cap) * d;
+                        for (int e = lane; e < d; e += 32) cv[e] = __fadd_rn(cv[e], delta_ctx[j * d + e]);
+                        __syncwarp();
+                    }
+                    for (int k = 0; k < S; ++k) {
+                        const int sid = k == 0 ? target : negs[static_cast<size_t>(i) * n_neg + k - 1];
+                        float* row = out_row(sid);
+                        for (int e = lane; e < d; e += 32) __stcg(row + e, __fadd_rn(__ldcg(row + e), delta_smp[k * d + e]));
+                        ++sw;
+                        __syncwarp();
+                    }
+                }
+            }
+            for (int s = 0; s < cap; ++s) {  // finish (trainer.cpp:71-75), slot order
+                if (slot_pos[s] >= 0) {
+                    row_put(in_row(slot_pos[s]), ring + s * d, d, lane);
+                    ++cw;
+                }
+            }
+            __syncwarp();
+        } else if (mode == kWindow) {
+            // train_sentence_window (trainer.cpp:257-290)
+            for (int i = 0; i < L; ++i) {
+                const int lo = max(0, i - wf), hh = min(L - 1, i + wf);
+                int n_ctx = 0;
+                for (int j = lo; j <= hh; ++j)
+                    if (j != i) { if (lane == 0) ctx_pos[n_ctx] = j; ++n_ctx; }
+                __syncwarp();
+                if (n_ctx == 0) continue;
+                for (int j = 0; j < n_ctx; ++j) { row_get(snap_ctx + j * d, in_row(ctx_pos[j]), d, lane); ++cr; }
+                __syncwarp();
+                const int target = ids[i];
+                for (int k = 0; k <= n_neg; ++k) {
+                    const int sid = k == 0 ? target : negs[static_cast<size_t>(i) * n_neg + k - 1];
+                    const float label = k == 0 ? 1.0f : 0.0f;
+                    row_get(sample, out_row(sid), d, lane);
+                    ++sr;
+                    __syncwarp();
+                    for (int j = 0; j < n_ctx; ++j) {
+                        float* cv = snap_ctx + j * d;
+                        const float f = dot_exact(cv, sample, d, lane);
+                        const float g = coeff_exact(f, label, alpha);
+                        pair_update_exact(cv, sample, g, d, lane);
+                        __syncwarp();
+                    }
+                    row_put(out_row(sid), sample, d, lane);
+                    ++sw;
+                    __syncwarp();
+                }
+                hits += static_cast<unsigned long long>(n_ctx) * n_neg;
+                for (int j = 0; j < n_ctx; ++j) {
+                    row_put(in_row(ctx_pos[j]), snap_ctx + j * d, d, lane);
+                    ++cw;
+                    __syncwarp();
+                }
+            }
+        } else {
+            // train_sentence_direct (trainer.cpp:292-328)
+            for (int i = 0; i < L; ++i) {
+                const int lo = max(0, i - wf), hh = min(L - 1, i + wf);
+                int n_ctx = 0;
+                for (int j = lo; j <= hh; ++j)
+                    if (j != i) { if (lane == 0) ctx_pos[n_ctx] = j; ++n_ctx; }
+                __syncwarp();
+                if (n_ctx == 0) continue;
+                const int target = ids[i];
+                for (int k = 0; k <= n_neg; ++k) {
+                    const int sid = k == 0 ? target : negs[static_cast<size_t>(i) * n_neg + k - 1];
+                    const float label = k == 0 ? 1.0f : 0.0f;
+                    for (int j = 0; j < n_ctx; ++j) {
+                        row_get(sample, out_row(sid), d, lane);
+                        ++sr;
+                        row_get(snap_ctx, in_row(ctx_pos[j]), d, lane);
+                        ++cr;
+                        __syncwarp();
+                        const float f = dot_exact(snap_ctx, sample, d, lane);
+                        const float g = coeff_exact(f, label, alpha);
+                        pair_update_exact(snap_ctx, sample, g, d, lane);
+                        __syncwarp();
+                        row_put(in_row(ctx_pos[j]), snap_ctx, d, lane);
+                        ++cw;
+                        row_put(out_row(sid), sample, d, lane);
+                        ++sw;
+                        __syncwarp();
+                    }
+                }
+            }
+        }
+    }
+    if (ctr != nullptr && lane == 0) {
+        atomicAdd(&ctr->context_reads, cr);
+        atomicAdd(&ctr->context_writes, cw);
+        atomicAdd(&ctr->sample_reads, sr);
+        atomicAdd(&ctr->sample_writes, sw);
+        atomicAdd(&ctr->ring_hits, hits);
+        atomicAdd(&ctr->words, words);
+        atomicAdd(&ctr->sentences, nsent);
+    }
+}
+
+// ------------------------------------------------------------- init kernel
+__device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// init_model (model.cpp:15-32): input[i] = (next_float() - 0.5f) * (1/d),
+// draw i of the "init" stream; output = 0; padding columns = 0.
+__global__ void k_init_model(ModelView m, uint64_t state0) {
+    const size_t n = static_cast<size_t>(m.vocab) * m.stride;
+    const float inv_dim = 1.0f / static_cast<float>(m.dim);
+    for (size_t x = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; x < n;
+         x += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t w = x / m.stride;
+        const int col = static_cast<int>(x - w * m.stride);
+        float v = 0.0f;
+        if (col < m.dim) {
+            const uint64_t i = w * static_cast<uint64_t>(m.dim) + col;
+            const uint64_t u = splitmix_mix(state0 + (i + 1) * 0x9e3779b97f4a7c15ULL);
+            const float nf = __fmul_rn(static_cast<float>(u >> 40), 0x1.0p-24f);
+            v = __fmul_rn(__fsub_rn(nf, 0.5f), inv_dim);
+        }
+        m.syn0[x] = v;
+        m.syn1[x] = 0.0f;
+    }
+}
+
+// --------------------------------------------------------------- dispatch
+struct K1Shape {
+    int lanes, vec;
+};
+
+template <int LANES, int VEC, int WF>
+cudaError_t launch_k1_wf(const ModelView& m, const BatchView& b, int n_neg, bool fast,
+                         DevCounters* ctr, cudaStream_t st) {
+    constexpr int GPW = 32 / LANES;
+    const int warps = (b.n_sentences + GPW - 1) / GPW;
+    const int blocks = (warps * 32 + kK1Threads - 1) / kK1Threads;
+    if (blocks == 0) return cudaSuccess;
+    if (fast) k1_lifetime<LANES, VEC, WF, true><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
+    else k1_lifetime<LANES, VEC, WF, false><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
+    return cudaGetLastError();
+}
+
+template <int LANES, int VEC>
+cudaError_t launch_k1_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
+                            DevCounters* ctr, cudaStream_t st) {
+    switch (wf) {
+    case 1: return launch_k1_wf<LANES, VEC, 1>(m, b, n_neg, fast, ctr, st);
+    case 2: return launch_k1_wf<LANES, VEC, 2>(m, b, n_neg, fast, ctr, st);
+    case 3: return launch_k1_wf<LANES, VEC, 3>(m, b, n_neg, fast, ctr, st);
+    case 4: return launch_k1_wf<LANES, VEC, 4>(m, b, n_neg, fast, ctr, st);
+    case 5: return launch_k1_wf<LANES, VEC, 5>(m, b, n_neg, fast, ctr, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+#define FW2V_K1_SHAPES(X) \
+    X(4, 1) X(4, 2) X(4, 4) X(8, 4) X(16, 4) X(8, 8) X(32, 4) X(16, 8) X(8, 16) \
+    X(32, 6) X(32, 8) X(32, 10) X(32, 12) X(32, 16)
+
+cudaError_t launch_k1(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf,
+                      bool fast, DevCounters* ctr, cudaStream_t st) {
+#define FW2V_CASE(L_, V_) \
+    if (lanes == L_ && vec == V_) return launch_k1_shape<L_, V_>(m, b, n_neg, wf, fast, ctr, st);
+    FW2V_K1_SHAPES(FW2V_CASE)
+#undef FW2V_CASE
+    return cudaErrorInvalidValue;
+}
+
+bool k1_shape_supported(int lanes, int vec) {
+#define FW2V_CASE(L_, V_) if (lanes == L_ && vec == V_) return true;
+    FW2V_K1_SHAPES(FW2V_CASE)
+#undef FW2V_CASE
+    return false;
+}
+
+size_t k2_smem_bytes(int dim, int wf, int n_neg) {
+    const int cap = 2 * wf + 1;
+    return sizeof(float) * static_cast<size_t>(dim) * (cap + 1 + 2 * (2 * wf) + 2 * (n_neg + 1));
+}
+
+cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf, int mode, bool serial,
+                      DevCounters* ctr, cudaStream_t st) {
+    if (wf < 1 || 2 * wf + 1 > kMaxRing) return cudaErrorInvalidValue;
+    if (b.n_sentences == 0) return cudaSuccess;
+    const size_t smem = k2_smem_bytes(m.dim, wf, n_neg);
+    static thread_local size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k2_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    const int grid = serial ? 1 : b.n_sentences;
+    k2_exact<<<grid, 32, smem, st>>>(m, b, n_neg, wf, mode, serial ? 1 : 0, ctr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st) {
+    k_init_model<<<148 * 8, 256, 0, st>>>(m, state0);
+    return cudaGetLastError();
+}
+
+} // namespace fw2v

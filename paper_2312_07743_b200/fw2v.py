@@ -1,0 +1,405 @@
+"""Python binding of the B200 FULL-W2V trainer C-ABI (include/fw2v.h).
+
+Thin ctypes layer over ``_lib/libfw2v.so``; the product is the C++/CUDA
+library, this module only marshals numpy arrays. There is no CPU training
+path: if the shared library is missing, importing the trainer raises, and on a
+machine without a CUDA device every training call fails with
+``FW2V_ERR_NO_DEVICE``.
+
+The surface mirrors the reference C++ API (``/root/reference/proj``):
+``TrainConfig`` (config.hpp:13-35), ``Trainer.train_corpus`` ≈ ``ringvec::train``
+(trainer.cpp:390), ``Trainer.train_sentences`` ≈ ``train_sentence``
+(trainer.cpp:332), and the batcher primitives ``keep_probs`` / ``table`` /
+``assemble_batch`` / ``lr_at`` / ``analytic_traffic`` with the reference's
+contracts (corpus.cpp:221, sampler.cpp:9-63, model.cpp:39, traffic.cpp:21).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(HERE, "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libfw2v.so")
+DROPIN_PATH = os.path.join(LIB_DIR, "libringvec_fw2v.so")
+
+REUSE_MODES = {"lifetime": 0, "window": 1, "none": 2, "window_snapshot": 3}
+SAMPLERS = {"reference": 0, "alias": 1}
+
+OK = 0
+ERR_NO_DEVICE = 66
+ERR_CUDA = 64
+ERR_UNSUPPORTED = 65
+ERR_BAD_ARGUMENT = 4
+ERR_BAD_CONFIG = 5
+
+# Every symbol include/fw2v.h declares (checked by tests/test_abi.py).
+EXPORTED = [
+    "fw2v_abi_version", "fw2v_last_error", "fw2v_config_default", "fw2v_validate_config",
+    "fw2v_device_count", "fw2v_create", "fw2v_destroy", "fw2v_get_model", "fw2v_set_model",
+    "fw2v_init_model", "fw2v_model_device", "fw2v_attach_model", "fw2v_row_stride",
+    "fw2v_train_corpus", "fw2v_train_sentences", "fw2v_plan_epoch", "fw2v_plan_info",
+    "fw2v_plan_run", "fw2v_plan_destroy", "fw2v_keep_probs", "fw2v_table_build",
+    "fw2v_assemble_batch", "fw2v_lr_at", "fw2v_analytic_traffic", "fw2v_corpus_synth_zipf",
+    "fw2v_corpus_view", "fw2v_corpus_free",
+]
+
+
+class Fw2vError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fw2v error {code}: {msg}")
+        self.code = code
+
+
+class CConfig(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("window", C.c_int32), ("negatives", C.c_int32), ("epochs", C.c_int32),
+        ("alpha0", C.c_float), ("subsample", C.c_double),
+        ("min_count", C.c_uint64), ("batch_sentences", C.c_uint64), ("max_sentence_len", C.c_uint64),
+        ("workers", C.c_int32), ("seed", C.c_uint64), ("reuse_mode", C.c_int32),
+        ("table_power", C.c_double), ("table_size", C.c_uint64), ("queue_capacity", C.c_uint64),
+        ("ignore_delimiters", C.c_int32),
+        ("device", C.c_int32), ("deterministic", C.c_int32), ("sampler", C.c_int32),
+        ("fast_sigmoid", C.c_int32), ("k1_lanes", C.c_int32), ("streams", C.c_int32),
+    ]
+
+
+class CCounters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("context_reads", "context_writes", "sample_reads",
+                                          "sample_writes", "ring_hits", "words", "sentences")]
+
+    def as_tuple(self):
+        return (self.context_reads, self.context_writes, self.sample_reads, self.sample_writes,
+                self.ring_hits)
+
+
+class CEpoch(C.Structure):
+    _fields_ = [("epoch", C.c_int32), ("words", C.c_uint64), ("seconds", C.c_double),
+                ("words_per_sec", C.c_double)]
+
+
+class CReport(C.Structure):
+    _fields_ = [
+        ("words_trained", C.c_uint64), ("sentences_trained", C.c_uint64), ("vocab_size", C.c_uint64),
+        ("wall_seconds", C.c_double), ("batching_words_per_sec", C.c_double), ("n_epochs", C.c_int32),
+        ("traffic", CCounters), ("analytic", CCounters), ("kernel_seconds", C.c_double),
+        ("h2d_bytes", C.c_uint64),
+    ]
+
+
+OBSERVER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_uint64)
+EPOCH_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(CEpoch))
+
+
+@dataclass
+class TrainConfig:
+    """ringvec::TrainConfig (config.hpp:13-35) plus the B200 extension."""
+
+    dim: int = 128
+    window: int = 5
+    negatives: int = 5
+    epochs: int = 20
+    alpha0: float = 0.025
+    subsample: float = 1e-4
+    min_count: int = 5
+    batch_sentences: int = 10000
+    max_sentence_len: int = 1000
+    workers: int = 0
+    seed: int = 1
+    reuse_mode: str = "lifetime"
+    table_power: float = 0.75
+    table_size: int = 10_000_000
+    queue_capacity: int = 0
+    ignore_delimiters: bool = True
+    # ---- B200 extension ----
+    device: int = 0
+    deterministic: int = -1
+    sampler: str = "reference"
+    fast_sigmoid: bool = True
+    k1_lanes: int = 0
+    streams: int = 0
+
+    @property
+    def context_width(self) -> int:
+        return (self.window + 1) // 2
+
+    def to_c(self) -> CConfig:
+        c = CConfig()
+        for f in fields(self):
+            v = getattr(self, f.name)
+            if f.name == "reuse_mode":
+                v = REUSE_MODES[v]
+            elif f.name == "sampler":
+                v = SAMPLERS[v]
+            elif isinstance(v, bool):
+                v = int(v)
+            setattr(c, f.name, v)
+        return c
+
+
+@dataclass
+class Report:
+    words_trained: int
+    sentences_trained: int
+    wall_seconds: float
+    batching_words_per_sec: float
+    traffic: tuple
+    analytic: tuple
+    h2d_bytes: int
+    epochs: list = field(default_factory=list)
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libfw2v.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `make lib` or __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    L.fw2v_last_error.restype = C.c_char_p
+    L.fw2v_lr_at.restype = C.c_float
+    L.fw2v_lr_at.argtypes = [C.c_uint64, C.c_uint64, C.c_float]
+    L.fw2v_assemble_batch.restype = C.c_int64
+    L.fw2v_row_stride.restype = C.c_int32
+    L.fw2v_destroy.restype = None
+    L.fw2v_plan_destroy.restype = None
+    L.fw2v_corpus_free.restype = None
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise Fw2vError(rc, lib().fw2v_last_error().decode())
+
+
+def _p(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    lib().fw2v_device_count(C.byref(n))
+    return n.value
+
+
+def row_stride(cfg: TrainConfig) -> int:
+    c = cfg.to_c()
+    return lib().fw2v_row_stride(C.byref(c))
+
+
+# ------------------------------------------------------------ batcher primitives
+def keep_probs(counts, threshold):
+    counts = np.ascontiguousarray(counts, np.uint64)
+    out = np.zeros(len(counts), np.float64)
+    on = lib().fw2v_keep_probs(_p(counts, C.c_uint64), len(counts), C.c_double(threshold), _p(out, C.c_double))
+    return out if on else None
+
+
+def table(counts, power, size):
+    counts = np.ascontiguousarray(counts, np.uint64)
+    out = np.zeros(size, np.int32)
+    _check(lib().fw2v_table_build(_p(counts, C.c_uint64), len(counts), C.c_double(power), C.c_uint64(size),
+                                  _p(out, C.c_int32)))
+    return out
+
+
+def assemble_batch(counts, offsets, ids, cursor, max_sentences, negatives, power, table_size, threshold,
+                   seed, a, b, c):
+    counts = np.ascontiguousarray(counts, np.uint64)
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    ids = np.ascontiguousarray(ids, np.int32)
+    cap = len(ids) + 1
+    o_ids = np.zeros(cap, np.int32)
+    o_off = np.zeros(len(offsets) + 1, np.uint64)
+    o_negs = np.zeros(cap * max(negatives, 1), np.int32)
+    cur = C.c_uint64(cursor)
+    n = lib().fw2v_assemble_batch(
+        _p(counts, C.c_uint64), len(counts), _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1),
+        _p(ids, C.c_int32), C.byref(cur), C.c_uint64(max_sentences), negatives, C.c_double(power),
+        C.c_uint64(table_size), C.c_double(threshold), C.c_uint64(seed), C.c_uint64(a), C.c_uint64(b),
+        C.c_uint64(c), _p(o_ids, C.c_int32), _p(o_off, C.c_uint64), _p(o_negs, C.c_int32))
+    if n < 0:
+        _check(-n)
+    off = o_off[: n + 1].copy()
+    w = int(off[-1])
+    return cur.value, off, o_ids[:w].copy(), o_negs[: w * negatives].copy()
+
+
+def lr_at(trained, total, alpha0):
+    return lib().fw2v_lr_at(trained, total, alpha0)
+
+
+def analytic_traffic(length, width, negatives, mode="lifetime"):
+    c = CCounters()
+    _check(lib().fw2v_analytic_traffic(C.c_uint64(length), width, negatives, REUSE_MODES[mode], C.byref(c)))
+    return c.as_tuple()
+
+
+# ------------------------------------------------------------ synthetic corpora
+class Corpus:
+    """Pre-subsampling corpus: vocabulary counts (id order), sentence offsets, ids."""
+
+    def __init__(self, counts, offsets, ids, _handle=None):
+        self.counts = counts
+        self.offsets = offsets
+        self.ids = ids
+        self._handle = _handle
+
+    @property
+    def n_sentences(self):
+        return len(self.offsets) - 1
+
+    def __del__(self):
+        if getattr(self, "_handle", None) is not None and _lib is not None:
+            _lib.fw2v_corpus_free(self._handle)
+            self._handle = None
+
+    def head(self, n_sentences: int) -> "Corpus":
+        """First n sentences (a bounded sample for CPU baselines); same vocabulary."""
+        off = np.ascontiguousarray(self.offsets[: n_sentences + 1])
+        return Corpus(self.counts, off, self.ids[: int(off[-1])])
+
+
+def synth_zipf(types, tokens, s=1.0, sentence_len=1000, min_count=5, threads=0) -> Corpus:
+    """Zipf corpus of the BASELINE.md shapes, generated by libfw2v (C++)."""
+    h = C.c_void_p()
+    _check(lib().fw2v_corpus_synth_zipf(C.c_uint64(types), C.c_uint64(tokens), C.c_double(s),
+                                        C.c_uint64(sentence_len), C.c_uint64(min_count), threads, C.byref(h)))
+    pc, po, pi = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint64)(), C.POINTER(C.c_int32)()
+    v, ns, ni = C.c_int32(), C.c_uint64(), C.c_uint64()
+    lib().fw2v_corpus_view(h, C.byref(pc), C.byref(v), C.byref(po), C.byref(ns), C.byref(pi), C.byref(ni))
+    counts = np.ctypeslib.as_array(pc, shape=(v.value,))
+    offsets = np.ctypeslib.as_array(po, shape=(ns.value + 1,))
+    ids = np.ctypeslib.as_array(pi, shape=(max(ni.value, 1),))[: ni.value]
+    return Corpus(counts, offsets, ids, _handle=h)
+
+
+TEXT8_SHAPE = dict(types=71_291, tokens=16_718_845)
+ONEBW_SHAPE = dict(types=555_514, tokens=804_269_957)
+
+
+# ------------------------------------------------------------ trainer
+class Trainer:
+    """One B200 trainer context (fw2v_ctx): model in HBM, host batcher, streams."""
+
+    def __init__(self, cfg: TrainConfig, counts):
+        self.cfg = cfg
+        self.counts = np.ascontiguousarray(counts, np.uint64)
+        self.vocab = len(self.counts)
+        self._c = cfg.to_c()
+        h = C.c_void_p()
+        _check(lib().fw2v_create(C.byref(self._c), _p(self.counts, C.c_uint64), self.vocab, C.byref(h)))
+        self._h = h
+        self.stride = row_stride(cfg)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fw2v_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def get_model(self):
+        d = self.cfg.dim
+        i = np.zeros((self.vocab, d), np.float32)
+        o = np.zeros((self.vocab, d), np.float32)
+        _check(lib().fw2v_get_model(self._h, _p(i, C.c_float), _p(o, C.c_float)))
+        return i, o
+
+    def set_model(self, inp=None, out=None):
+        pi = _p(np.ascontiguousarray(inp, np.float32), C.c_float) if inp is not None else None
+        po = _p(np.ascontiguousarray(out, np.float32), C.c_float) if out is not None else None
+        keep = (inp, out)  # noqa: F841 - keep buffers alive across the call
+        _check(lib().fw2v_set_model(self._h, pi, po))
+
+    def init_model(self, seed):
+        _check(lib().fw2v_init_model(self._h, C.c_uint64(seed)))
+
+    def model_device(self):
+        s0, s1, st = C.c_void_p(), C.c_void_p(), C.c_int32()
+        _check(lib().fw2v_model_device(self._h, C.byref(s0), C.byref(s1), C.byref(st)))
+        return s0.value, s1.value, st.value
+
+    def attach_model(self, syn0_ptr: int, syn1_ptr: int):
+        _check(lib().fw2v_attach_model(self._h, C.c_void_p(syn0_ptr), C.c_void_p(syn1_ptr)))
+
+    def train_sentences(self, offsets, ids, negatives, alphas, serial=True):
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        ids = np.ascontiguousarray(ids, np.int32)
+        negatives = np.ascontiguousarray(negatives, np.int32)
+        if negatives.size == 0:
+            negatives = np.zeros(1, np.int32)
+        alphas = np.ascontiguousarray(alphas, np.float32)
+        c = CCounters()
+        _check(lib().fw2v_train_sentences(self._h, _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1),
+                                          _p(ids, C.c_int32), _p(negatives, C.c_int32),
+                                          _p(alphas, C.c_float), int(serial), C.byref(c)))
+        return c
+
+    def train_corpus(self, corpus: Corpus, observer=None, on_epoch=None) -> Report:
+        offsets = np.ascontiguousarray(corpus.offsets, np.uint64)
+        ids = np.ascontiguousarray(corpus.ids, np.int32)
+        epochs = []
+
+        def _ep(_u, st):
+            e = st.contents
+            epochs.append(dict(epoch=e.epoch, words=e.words, seconds=e.seconds, words_per_sec=e.words_per_sec))
+            if on_epoch:
+                on_epoch(epochs[-1])
+
+        cb_obs = OBSERVER_FN(lambda _u, s, t: observer(s, t)) if observer else OBSERVER_FN()
+        cb_ep = EPOCH_FN(_ep)
+        rep = CReport()
+        _check(lib().fw2v_train_corpus(self._h, _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1),
+                                       _p(ids, C.c_int32), cb_obs, None, cb_ep, None, C.byref(rep)))
+        return Report(rep.words_trained, rep.sentences_trained, rep.wall_seconds, rep.batching_words_per_sec,
+                      rep.traffic.as_tuple(), rep.analytic.as_tuple(), rep.h2d_bytes, epochs)
+
+    def plan_epoch(self, corpus: Corpus, epoch: int = 0) -> "Plan":
+        offsets = np.ascontiguousarray(corpus.offsets, np.uint64)
+        ids = np.ascontiguousarray(corpus.ids, np.int32)
+        h = C.c_void_p()
+        _check(lib().fw2v_plan_epoch(self._h, _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1),
+                                     _p(ids, C.c_int32), epoch, C.byref(h)))
+        return Plan(self, h)
+
+
+class Plan:
+    """One epoch of batches resident in HBM (fw2v_plan)."""
+
+    def __init__(self, trainer: Trainer, handle):
+        self.trainer = trainer
+        self._h = handle
+        w, s, b, by = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        lib().fw2v_plan_info(handle, C.byref(w), C.byref(s), C.byref(b), C.byref(by))
+        self.words, self.sentences, self.batches, self.device_bytes = w.value, s.value, b.value, by.value
+
+    def run(self):
+        """Launches the plan's kernels; returns (device seconds, counters)."""
+        sec = C.c_double()
+        c = CCounters()
+        _check(lib().fw2v_plan_run(self.trainer._h, self._h, C.byref(sec), C.byref(c)))
+        return sec.value, c
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fw2v_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
