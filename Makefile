@@ -26,6 +26,10 @@ $(BUILD)/fw2v_kernels.o: $(SRC)/fw2v_kernels.cu $(SRC)/fw2v_device.cuh
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(BUILD)/ptxas_kernels.log || (cat $(BUILD)/ptxas_kernels.log; false)
 
+$(BUILD)/fw2v_snapshot.o: $(SRC)/fw2v_snapshot.cu $(SRC)/fw2v_device.cuh $(SRC)/fw2v_common.cuh
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(BUILD)/ptxas_snapshot.log || (cat $(BUILD)/ptxas_snapshot.log; false)
+
 $(BUILD)/fw2v_host.o: $(SRC)/fw2v_host.cpp include/fw2v.h $(SRC)/fw2v_device.cuh
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -c -o $@ $<
@@ -34,7 +38,7 @@ $(BUILD)/fw2v_corpus.o: $(SRC)/fw2v_corpus.cpp include/fw2v.h
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -O3 -c -o $@ $<
 
-$(LIB)/libfw2v.so: $(BUILD)/fw2v_kernels.o $(BUILD)/fw2v_host.o $(BUILD)/fw2v_corpus.o
+$(LIB)/libfw2v.so: $(BUILD)/fw2v_kernels.o $(BUILD)/fw2v_snapshot.o $(BUILD)/fw2v_host.o $(BUILD)/fw2v_corpus.o
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread -ldl -lrt
 

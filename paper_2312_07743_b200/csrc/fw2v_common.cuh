@@ -1,0 +1,91 @@
+// Device helpers shared by the FULL-W2V kernels (row I/O through L2, lane-group
+// reductions, the SGD coefficient).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fw2v {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kK1Threads = 128;
+
+// ------------------------------------------------------------------ row I/O
+// Model rows go through L2 only (ld.global.cg / st.global.cg): other SMs
+// update them concurrently (Hogwild), and L1 is not coherent within a launch.
+template <int VEC>
+struct Row {
+    __device__ __forceinline__ static void load(float (&v)[VEC], const float* p) {
+        if constexpr (VEC % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 4) {
+                float4 t = __ldcg(reinterpret_cast<const float4*>(p + i));
+                v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+            }
+        } else if constexpr (VEC % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 2) {
+                float2 t = __ldcg(reinterpret_cast<const float2*>(p + i));
+                v[i] = t.x; v[i + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) v[i] = __ldcg(p + i);
+        }
+    }
+    __device__ __forceinline__ static void store(float* p, const float (&v)[VEC]) {
+        if constexpr (VEC % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 4)
+                __stcg(reinterpret_cast<float4*>(p + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        } else if constexpr (VEC % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 2)
+                __stcg(reinterpret_cast<float2*>(p + i), make_float2(v[i], v[i + 1]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) __stcg(p + i, v[i]);
+        }
+    }
+};
+
+template <int VEC>
+__device__ __forceinline__ void vzero(float (&v)[VEC]) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = 0.0f;
+}
+
+template <int VEC>
+__device__ __forceinline__ void vcopy(float (&d)[VEC], const float (&s)[VEC]) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) d[i] = s[i];
+}
+
+template <int LANES>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+    for (int o = LANES / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// g = (label - sigma(clamp(f, -6, 6))) * alpha   (trainer.cpp:147, model.cpp:34-37)
+template <bool FAST>
+__device__ __forceinline__ float sgd_coeff(float f, float label, float alpha) {
+    f = fminf(fmaxf(f, -6.0f), 6.0f);
+    float sig;
+    if constexpr (FAST) {
+        sig = fmaf(0.5f, tanh_approx(0.5f * f), 0.5f);  // |err| < 1e-3 (SPEC fast-sigmoid bound)
+    } else {
+        sig = 1.0f / (1.0f + expf(-f));
+    }
+    return (label - sig) * alpha;
+}
+
+} // namespace fw2v

@@ -39,6 +39,9 @@ bool k1_shape_supported(int lanes, int vec);
 cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf, int mode, bool serial,
                       DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st);
+cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
+                       DevCounters* ctr, cudaStream_t st);
+bool k1s_supported(int lanes, int vec, int n_neg, int wf);
 } // namespace fw2v
 
 namespace {
@@ -421,6 +424,8 @@ struct fw2v_ctx {
         if (serial) return launch_k2(mv, bv, cfg.negatives, wf, cfg.reuse_mode, true, ctr, st);
         if (cfg.reuse_mode == kLifetime && shape.lanes > 0 && wf <= 5)
             return launch_k1(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, cfg.fast_sigmoid != 0, ctr, st);
+        if (cfg.reuse_mode == kWindowSnapshot && k1s_supported(shape.lanes, shape.vec, cfg.negatives, wf))
+            return launch_k1s(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, cfg.fast_sigmoid != 0, ctr, st);
         return launch_k2(mv, bv, cfg.negatives, wf, cfg.reuse_mode, false, ctr, st);
     }
 

@@ -73,7 +73,8 @@ def test_train_deterministic_bitwise(oracle, dim, window, n_neg, sub):
 @pytest.mark.parametrize("dim,lanes", [(8, 0), (12, 0), (16, 0), (32, 0), (64, 0), (128, 0), (128, 16),
                                        (128, 8), (256, 0), (300, 0), (512, 0)])
 @pytest.mark.parametrize("window", [2, 5, 7])
-def test_k1_single_sentence_semantics(oracle, dim, lanes, window):
+@pytest.mark.parametrize("mode", ["lifetime", "window_snapshot"])
+def test_k1_single_sentence_semantics(oracle, dim, lanes, window, mode):
     """K1 with one sentence per launch == reference order up to FP association
     (precise sigmoid); duplicates and negative collisions included."""
     counts, offsets, ids = random_corpus(6, 40, 25, seed=dim * 7 + window, min_len=1)
@@ -81,8 +82,8 @@ def test_k1_single_sentence_semantics(oracle, dim, lanes, window):
     n_neg = 5
     negs = fixed_negatives(int(offsets[-1]), n_neg, V, seed=9)
     alphas = np.full(len(offsets) - 1, 0.025, np.float32)
-    cfg = dict(dim=dim, window=window, negatives=n_neg, workers=4, deterministic=0, fast_sigmoid=False,
-               k1_lanes=lanes)
+    cfg = dict(dim=dim, window=window, negatives=n_neg, workers=4, reuse_mode=mode)
+    gcfg = dict(cfg, deterministic=0, fast_sigmoid=False, k1_lanes=lanes)
     ri, _ = oracle.init_model(V, dim, 5)
     ro = (ri[::-1] * 4.0).copy()
     gi0, go0 = ri.copy(), ro.copy()
@@ -92,7 +93,7 @@ def test_k1_single_sentence_semantics(oracle, dim, lanes, window):
         sl = ids[int(offsets[s]):int(offsets[s + 1])]
         ng = negs[int(offsets[s]) * n_neg:int(offsets[s + 1]) * n_neg]
         rc_total += np.array(oracle.train_sentences(ri, ro, o, sl, ng, alphas[s:s + 1], OConfig(**cfg)), np.uint64)
-    with _trainer(counts=counts, **cfg) as t:
+    with _trainer(counts=counts, **gcfg) as t:
         t.set_model(gi0, go0)
         tot = np.zeros(5, np.uint64)
         for s in range(len(offsets) - 1):
@@ -119,12 +120,12 @@ def test_k1_distinct_tokens_batch_equals_serial(oracle):
     counts = (100 + types - np.arange(types)).astype(np.uint64)
     n_neg = 0  # negatives would share rows across sentences
     alphas = np.full(n, 0.025, np.float32)
-    cfg = dict(dim=64, window=5, negatives=n_neg, workers=4, deterministic=0, fast_sigmoid=False)
+    cfg = dict(dim=64, window=5, negatives=n_neg, workers=4)
     ri, _ = oracle.init_model(types, 64, 3)
     ro = (ri[::-1] * 4.0).copy()
     gi0, go0 = ri.copy(), ro.copy()
     oracle.train_sentences(ri, ro, offsets, ids, np.zeros(0, np.int32), alphas, OConfig(**cfg))
-    with _trainer(counts=counts, **cfg) as t:
+    with _trainer(counts=counts, deterministic=0, fast_sigmoid=False, **cfg) as t:
         t.set_model(gi0, go0)
         t.train_sentences(offsets, ids, np.zeros(0, np.int32), alphas, serial=False)
         gi, go = t.get_model()
