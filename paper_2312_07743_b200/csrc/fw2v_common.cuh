@@ -50,6 +50,86 @@ struct Row {
     }
 };
 
+// Rows as float2 pairs (operands of the sm_100 packed FFMA2/FADD2).
+template <int H2>
+struct Row2 {
+    __device__ __forceinline__ static void load(float2 (&v)[H2], const float* p) {
+        if constexpr (H2 % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < H2; i += 2) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(p + 2 * i));
+                v[i] = make_float2(t.x, t.y);
+                v[i + 1] = make_float2(t.z, t.w);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < H2; ++i) v[i] = __ldcg(reinterpret_cast<const float2*>(p + 2 * i));
+        }
+    }
+    __device__ __forceinline__ static void store(float* p, const float2 (&v)[H2]) {
+        if constexpr (H2 % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < H2; i += 2)
+                __stcg(reinterpret_cast<float4*>(p + 2 * i), make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y));
+        } else {
+#pragma unroll
+            for (int i = 0; i < H2; ++i) __stcg(reinterpret_cast<float2*>(p + 2 * i), v[i]);
+        }
+    }
+    __device__ __forceinline__ static void load_shared(float2 (&v)[H2], const float* p) {
+        static_assert(H2 % 2 == 0, "16-byte shared slices");
+#pragma unroll
+        for (int i = 0; i < H2; i += 2) {
+            const float4 t = *reinterpret_cast<const float4*>(p + 2 * i);
+            v[i] = make_float2(t.x, t.y);
+            v[i + 1] = make_float2(t.z, t.w);
+        }
+    }
+    __device__ __forceinline__ static void store_shared(float* p, const float2 (&v)[H2]) {
+        static_assert(H2 % 2 == 0, "16-byte shared slices");
+#pragma unroll
+        for (int i = 0; i < H2; i += 2)
+            *reinterpret_cast<float4*>(p + 2 * i) = make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y);
+    }
+};
+
+template <int H2>
+__device__ __forceinline__ void vzero2(float2 (&v)[H2]) {
+#pragma unroll
+    for (int i = 0; i < H2; ++i) v[i] = make_float2(0.0f, 0.0f);
+}
+
+template <int H2>
+__device__ __forceinline__ void vcopy2(float2 (&d)[H2], const float2 (&s)[H2]) {
+#pragma unroll
+    for (int i = 0; i < H2; ++i) d[i] = s[i];
+}
+
+// Per-lane VEC-float slice of a row parked in shared memory.
+template <int VEC>
+__device__ __forceinline__ void stash_put(float* p, const float (&v)[VEC]) {
+    if constexpr (VEC % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) p[i] = v[i];
+    }
+}
+template <int VEC>
+__device__ __forceinline__ void stash_get(float (&v)[VEC], const float* p) {
+    if constexpr (VEC % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(p + i);
+            v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) v[i] = p[i];
+    }
+}
+
 template <int VEC>
 __device__ __forceinline__ void vzero(float (&v)[VEC]) {
 #pragma unroll

@@ -60,6 +60,12 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
     const size_t stride = static_cast<size_t>(m.stride);
     float* __restrict__ syn0 = m.syn0 + sub * VEC;
     float* __restrict__ syn1 = m.syn1 + sub * VEC;
+    // Positions >= tail stay resident until ContextRing::finish, which writes
+    // them in slot order; they are parked in shared memory until then.
+    constexpr int C = NCTX + 1;
+    extern __shared__ __align__(16) float k1_sh[];
+    float* stash = k1_sh + (threadIdx.x / LANES) * (C * LANES * VEC) + sub * VEC;
+    const int tail = L - C;
 
     // Window-relative ring: ctx[r] holds position i-WF+r (r < WF) or
     // i+1+(r-WF) (r >= WF); tgt holds position i. tok = -1 outside [0, L).
@@ -134,7 +140,9 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
         // Slide: position i-WF leaves the span and is written back.
         const int etok = tok[0];
         if (etok >= 0) {
-            Row<VEC>::store(syn0 + etok * stride, ctx[0]);
+            const int p = i - WF;
+            if (p >= tail) stash_put(stash + (p % C) * (LANES * VEC), ctx[0]);
+            else Row<VEC>::store(syn0 + etok * stride, ctx[0]);
             ++c_writes;
             if (inc_tok == etok) vcopy(inc, ctx[0]);  // load-after-evict forwarding
         }
@@ -149,12 +157,24 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
         vcopy(ctx[NCTX - 1], inc);
         tok[NCTX - 1] = inc_tok;
     }
-    // ContextRing::finish (trainer.cpp:71-75): residents still in registers.
+    // ContextRing::finish (trainer.cpp:71-75): residents written in slot order.
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
-        if (tok[r] >= 0) { Row<VEC>::store(syn0 + tok[r] * stride, ctx[r]); ++c_writes; }
+        const int p = r < WF ? Lmax - WF + r : Lmax + 1 + (r - WF);
+        if (tok[r] >= 0) { stash_put(stash + (p % C) * (LANES * VEC), ctx[r]); ++c_writes; }
     }
-    if (ttok >= 0) { Row<VEC>::store(syn0 + ttok * stride, tgt); ++c_writes; }
+    if (ttok >= 0) { stash_put(stash + (Lmax % C) * (LANES * VEC), tgt); ++c_writes; }
+    {
+        const int first = max(0, tail);
+        for (int s = 0; s < C; ++s) {
+            const int p = first + ((s - first % C) + C) % C;
+            if (p < L) {
+                float v[VEC];
+                stash_get(v, stash + s * (LANES * VEC));
+                Row<VEC>::store(syn0 + __ldg(ids + p) * stride, v);
+            }
+        }
+    }
 
     if (ctr != nullptr) {
         // One count per sentence: lane 0 of each group contributes.
@@ -484,8 +504,13 @@ cudaError_t launch_k1_wf(const ModelView& m, const BatchView& b, int n_neg, bool
     const int warps = (b.n_sentences + GPW - 1) / GPW;
     const int blocks = (warps * 32 + kK1Threads - 1) / kK1Threads;
     if (blocks == 0) return cudaSuccess;
-    if (fast) k1_lifetime<LANES, VEC, WF, true><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
-    else k1_lifetime<LANES, VEC, WF, false><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
+    constexpr int bytes = kK1Threads * (2 * WF + 1) * VEC * 4;  // finish stash per lane group
+    auto* kern = fast ? k1_lifetime<LANES, VEC, WF, true> : k1_lifetime<LANES, VEC, WF, false>;
+    if (bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<blocks, kK1Threads, bytes, st>>>(m, b, n_neg, ctr);
     return cudaGetLastError();
 }
 

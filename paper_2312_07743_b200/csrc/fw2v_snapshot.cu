@@ -2,22 +2,25 @@
 // rule; reference oracle: sweep_samples_snapshot,
 // trainer.cpp:158-205, ReuseMode::window_snapshot).
 //
-// Every (sample, context) pairing of a window is computed from the
-// window-entry values, so the (N+1) x 2W_f dots of a window are independent:
-//   1. the N+1 sample rows (syn1) are loaded once (128-bit, through L2);
-//   2. all dots are formed per lane (VEC columns each) and reduced across the
-//      LANES lanes of the sentence's group with ONE transposed butterfly: at each
-//      xor level a lane keeps half of its partial sums and sends the other half,
-//      so NV dots cost ~NV shuffles in total instead of NV*log2(LANES);
-//   3. each lane evaluates the sigmoid for the few dots it ended up owning and
-//      publishes g through 144 B of shared memory;
-//   4. sample deltas D_k = sum_r g_kr c_r and context updates c_r += sum_k g_kr s_k
-//      are register FMAs; samples are written back once per window.
+// Every (sample, context) pairing of a window is computed from window-entry
+// values, so the (N+1) x 2W_f dots of a window are independent:
+//   1. the N+1 sample rows (syn1) of window i+1 are prefetched with cp.async
+//      (16 B per lane, L2 only) into shared memory while window i computes;
+//   2. all dots are formed per lane on VEC columns with packed FFMA2
+//      (sm_100 fma.rn.f32x2) and reduced across the LANES lanes of the
+//      sentence's group with ONE transposed butterfly: at each xor level a lane
+//      keeps half of its partial sums and sends the other half, so NV dots cost
+//      ~NV shuffles in total instead of NV*log2(LANES);
+//   3. each lane evaluates the sigmoid for the dots it ended up owning and
+//      publishes g as (g, g) pairs in shared memory;
+//   4. sample deltas D_k = sum_r g_kr c_r and context updates
+//      c_r += sum_k g_kr s_k are FFMA2 on registers; samples are written once
+//      per window (row += delta, trainer.cpp:198-204).
 // The 2W_f+1 ring of syn0 rows (ContextRing, trainer.cpp:32-102) stays in
-// registers for the sentence's lifetime and slides by register renaming, as
-// in K1. Samples are processed in chunks of NC rows (MULTI: N+1 > NC), with
-// context deltas accumulated across chunks so all chunks see window-entry
-// context values.
+// registers for the sentence's lifetime and slides by register renaming.
+// Positions that the reference keeps resident until finish() (the last 2W_f+1)
+// are parked in shared memory and written back in ring-slot order, so each
+// sentence's global write sequence is the reference's.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,7 +32,7 @@ namespace fw2v {
 
 // Transposed butterfly over the lanes of a group (offsets O, O/2, ..., 1).
 // v[0..N) in, v[0..final) out; slot j of lane l then holds the full group sum
-// of the original index given by the same plan run on an index array.
+// of the original index given by running plan() on an index array.
 template <int O, int N>
 struct Butterfly {
     static constexpr int H = N / 2;
@@ -64,15 +67,36 @@ struct Butterfly {
     }
 };
 
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int LANES, int VEC, int WF, int NC>
+struct K1sSmem {
+    static constexpr int NCTX = 2 * WF;
+    static constexpr int C = 2 * WF + 1;
+    static constexpr int NV = NC * NCTX;
+    static constexpr int STRIDE = LANES * VEC;
+    // per group: g pairs, sample prefetch buffer, finish stash
+    static constexpr int kGroupFloats = 2 * NV + NC * STRIDE + C * STRIDE;
+    static constexpr int kBlockBytes = (kK1Threads / LANES) * kGroupFloats * 4;
+};
+
 template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
 __global__ void __launch_bounds__(kK1Threads)
 k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) {
-    constexpr int NCTX = 2 * WF;
-    constexpr int NV = NC * NCTX;
+    static_assert(VEC % 4 == 0, "K1s stages 16-byte slices");
+    using SM = K1sSmem<LANES, VEC, WF, NC>;
+    constexpr int NCTX = SM::NCTX;
+    constexpr int C = SM::C;
+    constexpr int NV = SM::NV;
+    constexpr int H2 = VEC / 2;
     constexpr int GPW = 32 / LANES;
     using BF = Butterfly<LANES / 2, NV>;
     constexpr int NF = BF::final_count();
-    __shared__ float gsh[kK1Threads / 32][GPW][NV];
+    extern __shared__ __align__(16) float k1s_sh[];
 
     const int lane = threadIdx.x & 31;
     const int sub = lane & (LANES - 1);
@@ -80,7 +104,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int sent = warp * GPW + grp;
     const bool has = sent < b.n_sentences;
-    float* gmy = gsh[threadIdx.x >> 5][grp];
+    float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
+    float2* g2 = reinterpret_cast<float2*>(gsh);
+    float* sbuf = gsh + 2 * NV + sub * VEC;                     // + q*STRIDE
+    float* stash = gsh + 2 * NV + NC * SM::STRIDE + sub * VEC;  // + slot*STRIDE
 
     uint32_t beg = 0, len = 0;
     float alpha = 0.0f;
@@ -98,8 +125,8 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     const size_t stride = static_cast<size_t>(m.stride);
     float* __restrict__ syn0 = m.syn0 + sub * VEC;
     float* __restrict__ syn1 = m.syn1 + sub * VEC;
+    const int tail = L - C;  // positions >= tail stay resident until finish()
 
-    // Which (sample, context) dot each of this lane's final butterfly slots holds.
     int slot_q[NF], slot_r[NF], slot_m[NF];
     {
         int idx[NV];
@@ -108,28 +135,46 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         BF::plan(idx, sub);
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-            slot_m[j] = idx[j];
             slot_q[j] = idx[j] / NCTX;
             slot_r[j] = idx[j] - slot_q[j] * NCTX;
+            slot_m[j] = slot_r[j] * NC + slot_q[j];  // g pairs are stored context-major
         }
     }
-    float ctx[NCTX][VEC];
+
+    float2 ctx[NCTX][H2];
     int tok[NCTX];
-    float tgt[VEC];
+    float2 tgt[H2];
     int ttok = L > 0 ? __ldg(ids) : -1;
-    if (ttok >= 0) Row<VEC>::load(tgt, syn0 + ttok * stride); else vzero(tgt);
+    if (ttok >= 0) Row2<H2>::load(tgt, syn0 + ttok * stride); else vzero2(tgt);
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
         const int p = r - WF + 1;
         tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
-        if (tok[r] >= 0) Row<VEC>::load(ctx[r], syn0 + tok[r] * stride); else vzero(ctx[r]);
+        if (tok[r] >= 0) Row2<H2>::load(ctx[r], syn0 + tok[r] * stride); else vzero2(ctx[r]);
     }
     unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
-    unsigned c_writes = 0, s_rw = 0, pairs = 0;
+    unsigned s_rw = 0, pairs = 0;
 
     // Negatives of the current window, one per lane (lane q holds negative q).
     int negreg = (sub < n_neg && L >= 2) ? __ldg(negs + sub) : -1;
-    float dctx[MULTI ? NCTX : 1][VEC];
+    // Sample ids of the first chunk of the previous window (stale-prefetch check).
+    int psid[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) psid[q] = -1;
+
+    auto prefetch = [&](int target, int negv, bool active) {
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const int nb = __shfl_sync(kFull, negv, (q - 1) & (LANES - 1), LANES);
+            const int s = q == 0 ? target : nb;
+            if (active && q <= n_neg && s >= 0) {
+#pragma unroll
+                for (int e = 0; e < VEC; e += 4) cp_async16(sbuf + q * SM::STRIDE + e, syn1 + s * stride + e);
+            }
+        }
+    };
+    if (!MULTI) prefetch(ttok, negreg, L >= 2);  // window 0's samples
+    float2 dctx[MULTI ? NCTX : 1][H2];
 
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
@@ -139,25 +184,43 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         for (int r = 0; r < NCTX; ++r) vmask |= (tok[r] >= 0 ? 1u : 0u) << r;
         const int q_in = i + 1 + WF;
         const int inc_tok = q_in < L ? __ldg(ids + q_in) : -1;
-        float inc[VEC];
-        if (inc_tok >= 0) Row<VEC>::load(inc, syn0 + inc_tok * stride); else vzero(inc);
+        float2 inc[H2];
+        if (inc_tok >= 0) Row2<H2>::load(inc, syn0 + inc_tok * stride); else vzero2(inc);
         c_reads += inc_tok >= 0;
         const int negnext = (sub < n_neg && i + 1 < L) ? __ldg(negs + static_cast<size_t>(i + 1) * n_neg + sub) : -1;
         if constexpr (MULTI) {
 #pragma unroll
-            for (int r = 0; r < NCTX; ++r) vzero(dctx[r]);
+            for (int r = 0; r < NCTX; ++r) vzero2(dctx[r]);
         }
 
         for (int ch = 0; ch * NC <= n_neg; ++ch) {
             int sid[NC];
-            float S[NC][VEC];
+            float2 S[NC][H2];
 #pragma unroll
             for (int q = 0; q < NC; ++q) {
                 const int kk = ch * NC + q;
                 const int nb = __shfl_sync(kFull, negreg, (kk - 1) & (LANES - 1), LANES);
                 const int s = kk == 0 ? ttok : nb;
                 sid[q] = (wact && kk <= n_neg) ? s : -1;
-                if (sid[q] >= 0) Row<VEC>::load(S[q], syn1 + sid[q] * stride); else vzero(S[q]);
+            }
+            if (!MULTI) {
+                // Staged by cp.async during the previous window; rows the previous
+                // window wrote after the prefetch was issued are re-read.
+                cp_async_wait_all();
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    bool stale = false;
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) stale |= sid[q] == psid[j];
+                    if (sid[q] < 0) vzero2(S[q]);
+                    else if (stale) Row2<H2>::load(S[q], syn1 + sid[q] * stride);
+                    else Row2<H2>::load_shared(S[q], sbuf + q * SM::STRIDE);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    if (sid[q] >= 0) Row2<H2>::load(S[q], syn1 + sid[q] * stride); else vzero2(S[q]);
+                }
             }
             unsigned dup = 0;
 #pragma unroll
@@ -171,64 +234,74 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             for (int q = 0; q < NC; ++q)
 #pragma unroll
                 for (int r = 0; r < NCTX; ++r) {
-                    float acc = 0.0f;
+                    float2 acc = __fmul2_rn(ctx[r][0], S[q][0]);
 #pragma unroll
-                    for (int e = 0; e < VEC; ++e) acc = fmaf(ctx[r][e], S[q][e], acc);
-                    P[q * NCTX + r] = acc;
+                    for (int h = 1; h < H2; ++h) acc = __ffma2_rn(ctx[r][h], S[q][h], acc);
+                    P[q * NCTX + r] = acc.x + acc.y;
                 }
             BF::reduce(P, sub);
 
-            // 3. sigmoid on owned slots, publish g.
+            // Next window's first chunk: its ids have arrived by now.
+            if (!MULTI && i + 1 < Lmax) prefetch(tok[WF], negnext, i + 1 < L && L >= 2);
+
+            // 3. sigmoid on owned slots, publish g pairs.
 #pragma unroll
             for (int j = 0; j < NF; ++j) {
                 const int kk = ch * NC + slot_q[j];
                 const bool valid = wact && kk <= n_neg && ((vmask >> slot_r[j]) & 1u);
                 const float g = valid ? sgd_coeff<FAST>(P[j], kk == 0 ? 1.0f : 0.0f, alpha) : 0.0f;
-                gmy[slot_m[j]] = g;
+                g2[slot_m[j]] = make_float2(g, g);  // context-major: [r][q]
             }
-            __syncwarp();
-            float G[NV];
-#pragma unroll
-            for (int x = 0; x < NV; ++x) G[x] = gmy[x];
             __syncwarp();
 
-            // 4. sample deltas from window-entry contexts; context updates from
-            //    window-entry samples.
-            float D[NC][VEC];
+            // 4. context-major sweep: with r fixed, sample deltas take the
+            //    window-entry c_r, then c_r takes the window-entry samples, so
+            //    each (g, g) pair is loaded once and used twice.
+            float2 D[NC][H2];
 #pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                vzero(D[q]);
+            for (int q = 0; q < NC; ++q) vzero2(D[q]);
 #pragma unroll
-                for (int r = 0; r < NCTX; ++r)
+            for (int r = 0; r < NCTX; ++r) {
+                float2 G[NC];
 #pragma unroll
-                    for (int e = 0; e < VEC; ++e) D[q][e] = fmaf(G[q * NCTX + r], ctx[r][e], D[q][e]);
-            }
-#pragma unroll
-            for (int r = 0; r < NCTX; ++r)
+                for (int q = 0; q < NC; q += 2) {
+                    const float4 t = *reinterpret_cast<const float4*>(g2 + r * NC + q);
+                    G[q] = make_float2(t.x, t.y);
+                    if (q + 1 < NC) G[q + 1] = make_float2(t.z, t.w);
+                }
 #pragma unroll
                 for (int q = 0; q < NC; ++q)
 #pragma unroll
-                    for (int e = 0; e < VEC; ++e) {
-                        if constexpr (MULTI) dctx[r][e] = fmaf(G[q * NCTX + r], S[q][e], dctx[r][e]);
-                        else ctx[r][e] = fmaf(G[q * NCTX + r], S[q][e], ctx[r][e]);
+                    for (int h = 0; h < H2; ++h) D[q][h] = __ffma2_rn(G[q], ctx[r][h], D[q][h]);
+#pragma unroll
+                for (int q = 0; q < NC; ++q)
+#pragma unroll
+                    for (int h = 0; h < H2; ++h) {
+                        if constexpr (MULTI) dctx[r][h] = __ffma2_rn(G[q], S[q][h], dctx[r][h]);
+                        else ctx[r][h] = __ffma2_rn(G[q], S[q][h], ctx[r][h]);
                     }
-            // Write back (row += delta, trainer.cpp:198-204). A repeated id re-reads
-            // the row so both deltas land, as in the reference.
+            }
+            __syncwarp();
+            // Write back; a repeated id re-reads the row so both deltas land.
 #pragma unroll
             for (int q = 0; q < NC; ++q) {
                 if (sid[q] < 0) continue;
                 float* row = syn1 + sid[q] * stride;
-                if ((dup >> q) & 1u) Row<VEC>::load(S[q], row);
+                if ((dup >> q) & 1u) Row2<H2>::load(S[q], row);
 #pragma unroll
-                for (int e = 0; e < VEC; ++e) S[q][e] += D[q][e];
-                Row<VEC>::store(row, S[q]);
+                for (int h = 0; h < H2; ++h) S[q][h] = __fadd2_rn(S[q][h], D[q][h]);
+                Row2<H2>::store(row, S[q]);
+            }
+            if (ch == 0) {
+#pragma unroll
+                for (int q = 0; q < NC; ++q) psid[q] = sid[q];
             }
         }
         if constexpr (MULTI) {
 #pragma unroll
             for (int r = 0; r < NCTX; ++r)
 #pragma unroll
-                for (int e = 0; e < VEC; ++e) ctx[r][e] += dctx[r][e];
+                for (int h = 0; h < H2; ++h) ctx[r][h] = __fadd2_rn(ctx[r][h], dctx[r][h]);
         }
         if (wact) {
             s_rw += static_cast<unsigned>(n_neg + 1);
@@ -238,40 +311,55 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         // Slide the ring (ContextRing::advance, trainer.cpp:55-69).
         const int etok = tok[0];
         if (etok >= 0) {
-            Row<VEC>::store(syn0 + etok * stride, ctx[0]);
-            ++c_writes;
-            if (inc_tok == etok) vcopy(inc, ctx[0]);
+            const int p = i - WF;
+            if (p >= tail) Row2<H2>::store_shared(stash + (p % C) * SM::STRIDE, ctx[0]);
+            else Row2<H2>::store(syn0 + etok * stride, ctx[0]);
+            if (inc_tok == etok) vcopy2(inc, ctx[0]);
         }
 #pragma unroll
-        for (int r = 0; r < WF - 1; ++r) { vcopy(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
-        vcopy(ctx[WF - 1], tgt);
+        for (int r = 0; r < WF - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
+        vcopy2(ctx[WF - 1], tgt);
         tok[WF - 1] = act ? ttok : -1;
-        vcopy(tgt, ctx[WF]);
+        vcopy2(tgt, ctx[WF]);
         ttok = tok[WF];
 #pragma unroll
-        for (int r = WF; r < NCTX - 1; ++r) { vcopy(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
-        vcopy(ctx[NCTX - 1], inc);
+        for (int r = WF; r < NCTX - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
+        vcopy2(ctx[NCTX - 1], inc);
         tok[NCTX - 1] = inc_tok;
         negreg = negnext;
     }
+    // ContextRing::finish (trainer.cpp:71-75): residents in slot order.
+    {
+        const int i_end = Lmax;  // registers hold positions i_end-WF .. i_end+WF
 #pragma unroll
-    for (int r = 0; r < NCTX; ++r) {
-        if (tok[r] >= 0) { Row<VEC>::store(syn0 + tok[r] * stride, ctx[r]); ++c_writes; }
+        for (int r = 0; r < NCTX; ++r) {
+            const int p = r < WF ? i_end - WF + r : i_end + 1 + (r - WF);
+            if (tok[r] >= 0) Row2<H2>::store_shared(stash + (p % C) * SM::STRIDE, ctx[r]);
+        }
+        if (ttok >= 0) Row2<H2>::store_shared(stash + (i_end % C) * SM::STRIDE, tgt);
+        const int first = max(0, tail);
+        for (int s = 0; s < C; ++s) {
+            // the resident position in slot s: first + ((s - first) mod C), if < L
+            const int p = first + ((s - first % C) + C) % C;
+            if (p < L) {
+                float2 v[H2];
+                Row2<H2>::load_shared(v, stash + s * SM::STRIDE);
+                Row2<H2>::store(syn0 + __ldg(ids + p) * stride, v);
+            }
+        }
     }
-    if (ttok >= 0) { Row<VEC>::store(syn0 + ttok * stride, tgt); ++c_writes; }
 
     if (ctr != nullptr) {
         const bool lead = has && sub == 0;
         const unsigned hits = (L >= 2) ? pairs - static_cast<unsigned>(L) : 0u;
         const unsigned v0 = __reduce_add_sync(kFull, lead ? c_reads : 0u);
-        const unsigned v1 = __reduce_add_sync(kFull, lead ? c_writes : 0u);
         const unsigned v2 = __reduce_add_sync(kFull, lead ? s_rw : 0u);
         const unsigned v4 = __reduce_add_sync(kFull, lead ? hits : 0u);
         const unsigned v5 = __reduce_add_sync(kFull, lead ? static_cast<unsigned>(L) : 0u);
         const unsigned v6 = __reduce_add_sync(kFull, lead ? 1u : 0u);
         if (lane == 0) {
             atomicAdd(&ctr->context_reads, v0);
-            atomicAdd(&ctr->context_writes, v1);
+            atomicAdd(&ctr->context_writes, v5);  // every position is written back exactly once
             atomicAdd(&ctr->sample_reads, v2);
             atomicAdd(&ctr->sample_writes, v2);
             atomicAdd(&ctr->ring_hits, v4);
@@ -282,6 +370,21 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 }
 
 // ------------------------------------------------------------------ dispatch
+template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
+cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, int n_neg, DevCounters* ctr,
+                            cudaStream_t st) {
+    constexpr int bytes = K1sSmem<LANES, VEC, WF, NC>::kBlockBytes;
+    auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MULTI, FAST>;
+    static bool configured = false;  // benign race: idempotent attribute set
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    kern<<<blocks, kK1Threads, bytes, st>>>(m, b, n_neg, ctr);
+    return cudaGetLastError();
+}
+
 template <int LANES, int VEC, int WF, int NC>
 cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
                           cudaStream_t st) {
@@ -291,13 +394,11 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
     if (blocks == 0) return cudaSuccess;
     const bool multi = n_neg + 1 > NC;
     if (multi) {
-        if (fast) k1s_snapshot<LANES, VEC, WF, NC, true, true><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
-        else k1s_snapshot<LANES, VEC, WF, NC, true, false><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
-    } else {
-        if (fast) k1s_snapshot<LANES, VEC, WF, NC, false, true><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
-        else k1s_snapshot<LANES, VEC, WF, NC, false, false><<<blocks, kK1Threads, 0, st>>>(m, b, n_neg, ctr);
+        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, true, true>(blocks, m, b, n_neg, ctr, st)
+                    : launch_k1s_inst<LANES, VEC, WF, NC, true, false>(blocks, m, b, n_neg, ctr, st);
     }
-    return cudaGetLastError();
+    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, false, true>(blocks, m, b, n_neg, ctr, st)
+                : launch_k1s_inst<LANES, VEC, WF, NC, false, false>(blocks, m, b, n_neg, ctr, st);
 }
 
 template <int LANES, int VEC>
@@ -313,7 +414,7 @@ cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, 
     }
 }
 
-#define FW2V_K1S_SHAPES(X) X(16, 4) X(32, 4) X(16, 8) X(32, 8) X(32, 10)
+#define FW2V_K1S_SHAPES(X) X(16, 4) X(32, 4) X(32, 8)
 
 // Requires n_neg <= LANES (negatives are distributed one per lane).
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
