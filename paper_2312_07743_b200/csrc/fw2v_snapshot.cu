@@ -122,7 +122,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 
     const int32_t* __restrict__ ids = b.ids + beg;
     const int32_t* __restrict__ negs = b.negs + static_cast<size_t>(beg) * n_neg;
-    const size_t stride = static_cast<size_t>(m.stride);
+    // Row offsets use the compile-time stride (host checks |V| * stride < 2^31).
     float* __restrict__ syn0 = m.syn0 + sub * VEC;
     float* __restrict__ syn1 = m.syn1 + sub * VEC;
     const int tail = L - C;  // positions >= tail stay resident until finish()
@@ -145,12 +145,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     int tok[NCTX];
     float2 tgt[H2];
     int ttok = L > 0 ? __ldg(ids) : -1;
-    if (ttok >= 0) Row2<H2>::load(tgt, syn0 + ttok * stride); else vzero2(tgt);
+    if (ttok >= 0) Row2<H2>::load(tgt, syn0 + ttok * SM::STRIDE); else vzero2(tgt);
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
         const int p = r - WF + 1;
         tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
-        if (tok[r] >= 0) Row2<H2>::load(ctx[r], syn0 + tok[r] * stride); else vzero2(ctx[r]);
+        if (tok[r] >= 0) Row2<H2>::load(ctx[r], syn0 + tok[r] * SM::STRIDE); else vzero2(ctx[r]);
     }
     unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
     unsigned s_rw = 0, pairs = 0;
@@ -160,16 +160,23 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     // Sample ids of the first chunk of the previous window (stale-prefetch check).
     int psid[NC];
 #pragma unroll
-    for (int q = 0; q < NC; ++q) psid[q] = -1;
+    for (int q = 0; q < NC; ++q) psid[q] = -100;  // sentinels never equal a live or empty sample id
 
+    {
+        const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+#pragma unroll
+            for (int e = 0; e < VEC; e += 4) *reinterpret_cast<float4*>(sbuf + q * SM::STRIDE + e) = z;
+    }
     auto prefetch = [&](int target, int negv, bool active) {
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-            const int nb = __shfl_sync(kFull, negv, (q - 1) & (LANES - 1), LANES);
+            const int nb = __shfl_sync(kFull, negv, (q + LANES - 1) & (LANES - 1), LANES);
             const int s = q == 0 ? target : nb;
             if (active && q <= n_neg && s >= 0) {
 #pragma unroll
-                for (int e = 0; e < VEC; e += 4) cp_async16(sbuf + q * SM::STRIDE + e, syn1 + s * stride + e);
+                for (int e = 0; e < VEC; e += 4) cp_async16(sbuf + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
             }
         }
     };
@@ -185,7 +192,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         const int q_in = i + 1 + WF;
         const int inc_tok = q_in < L ? __ldg(ids + q_in) : -1;
         float2 inc[H2];
-        if (inc_tok >= 0) Row2<H2>::load(inc, syn0 + inc_tok * stride); else vzero2(inc);
+        if (inc_tok >= 0) Row2<H2>::load(inc, syn0 + inc_tok * SM::STRIDE); else vzero2(inc);
         c_reads += inc_tok >= 0;
         const int negnext = (sub < n_neg && i + 1 < L) ? __ldg(negs + static_cast<size_t>(i + 1) * n_neg + sub) : -1;
         if constexpr (MULTI) {
@@ -193,40 +200,49 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             for (int r = 0; r < NCTX; ++r) vzero2(dctx[r]);
         }
 
-        for (int ch = 0; ch * NC <= n_neg; ++ch) {
+        const int n_chunks = MULTI ? (n_neg + NC) / NC : 1;
+        for (int ch = 0; ch < n_chunks; ++ch) {
+            const int kbase = MULTI ? ch * NC : 0;
             int sid[NC];
             float2 S[NC][H2];
 #pragma unroll
             for (int q = 0; q < NC; ++q) {
-                const int kk = ch * NC + q;
-                const int nb = __shfl_sync(kFull, negreg, (kk - 1) & (LANES - 1), LANES);
+                const int kk = kbase + q;
+                const int src = MULTI ? ((kk - 1) & (LANES - 1)) : ((q + LANES - 1) & (LANES - 1));
+                const int nb = __shfl_sync(kFull, negreg, src, LANES);
                 const int s = kk == 0 ? ttok : nb;
-                sid[q] = (wact && kk <= n_neg) ? s : -1;
+                sid[q] = (wact && kk <= n_neg) ? s : -1 - q;  // empty slots: distinct negative ids
             }
-            if (!MULTI) {
-                // Staged by cp.async during the previous window; rows the previous
-                // window wrote after the prefetch was issued are re-read.
+            if constexpr (!MULTI) {
+                // Staged by cp.async during the previous window (slots without a
+                // sample hold finite stale rows and get g = 0). Rows the previous
+                // window rewrote after the prefetch was issued are re-read.
                 cp_async_wait_all();
 #pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    bool stale = false;
+                for (int q = 0; q < NC; ++q) Row2<H2>::load_shared(S[q], sbuf + q * SM::STRIDE);
+                bool stale = false;
+#pragma unroll
+                for (int q = 0; q < NC; ++q)
 #pragma unroll
                     for (int j = 0; j < NC; ++j) stale |= sid[q] == psid[j];
-                    if (sid[q] < 0) vzero2(S[q]);
-                    else if (stale) Row2<H2>::load(S[q], syn1 + sid[q] * stride);
-                    else Row2<H2>::load_shared(S[q], sbuf + q * SM::STRIDE);
+                if (stale) {
+#pragma unroll
+                    for (int q = 0; q < NC; ++q) {
+                        bool st = false;
+#pragma unroll
+                        for (int j = 0; j < NC; ++j) st |= sid[q] == psid[j];
+                        if (st && sid[q] >= 0) Row2<H2>::load(S[q], syn1 + sid[q] * SM::STRIDE);
+                    }
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    if (sid[q] >= 0) Row2<H2>::load(S[q], syn1 + sid[q] * stride); else vzero2(S[q]);
-                }
+                for (int q = 0; q < NC; ++q) Row2<H2>::load(S[q], syn1 + max(sid[q], 0) * SM::STRIDE);
             }
             unsigned dup = 0;
 #pragma unroll
             for (int q = 1; q < NC; ++q)
 #pragma unroll
-                for (int j = 0; j < q; ++j) dup |= (sid[q] >= 0 && sid[q] == sid[j] ? 1u : 0u) << q;
+                for (int j = 0; j < q; ++j) dup |= (sid[q] == sid[j] ? 1u : 0u) << q;
 
             // 1-2. all dots of the chunk, then one transposed butterfly.
             float P[NV];
@@ -283,18 +299,27 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             }
             __syncwarp();
             // Write back; a repeated id re-reads the row so both deltas land.
+            if (dup == 0) {
 #pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                if (sid[q] < 0) continue;
-                float* row = syn1 + sid[q] * stride;
-                if ((dup >> q) & 1u) Row2<H2>::load(S[q], row);
+                for (int q = 0; q < NC; ++q) {
 #pragma unroll
-                for (int h = 0; h < H2; ++h) S[q][h] = __fadd2_rn(S[q][h], D[q][h]);
-                Row2<H2>::store(row, S[q]);
+                    for (int h = 0; h < H2; ++h) S[q][h] = __fadd2_rn(S[q][h], D[q][h]);
+                    if (sid[q] >= 0) Row2<H2>::store(syn1 + sid[q] * SM::STRIDE, S[q]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    if (sid[q] < 0) continue;
+                    float* row = syn1 + sid[q] * SM::STRIDE;
+                    if ((dup >> q) & 1u) Row2<H2>::load(S[q], row);
+#pragma unroll
+                    for (int h = 0; h < H2; ++h) S[q][h] = __fadd2_rn(S[q][h], D[q][h]);
+                    Row2<H2>::store(row, S[q]);
+                }
             }
             if (ch == 0) {
 #pragma unroll
-                for (int q = 0; q < NC; ++q) psid[q] = sid[q];
+                for (int q = 0; q < NC; ++q) psid[q] = sid[q] >= 0 ? sid[q] : -100;
             }
         }
         if constexpr (MULTI) {
@@ -313,7 +338,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         if (etok >= 0) {
             const int p = i - WF;
             if (p >= tail) Row2<H2>::store_shared(stash + (p % C) * SM::STRIDE, ctx[0]);
-            else Row2<H2>::store(syn0 + etok * stride, ctx[0]);
+            else Row2<H2>::store(syn0 + etok * SM::STRIDE, ctx[0]);
             if (inc_tok == etok) vcopy2(inc, ctx[0]);
         }
 #pragma unroll
@@ -344,7 +369,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             if (p < L) {
                 float2 v[H2];
                 Row2<H2>::load_shared(v, stash + s * SM::STRIDE);
-                Row2<H2>::store(syn0 + __ldg(ids + p) * stride, v);
+                Row2<H2>::store(syn0 + __ldg(ids + p) * SM::STRIDE, v);
             }
         }
     }
