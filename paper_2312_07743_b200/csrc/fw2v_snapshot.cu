@@ -72,6 +72,8 @@ __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+constexpr int kPrefetchWindows = 16;
 
 template <int LANES, int VEC, int WF, int NC>
 struct K1sSmem {
@@ -85,7 +87,7 @@ struct K1sSmem {
 };
 
 template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
-__global__ void __launch_bounds__(kK1Threads)
+__global__ void __launch_bounds__(kK1Threads, (VEC >= 8 ? 1 : 3))
 k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) {
     static_assert(VEC % 4 == 0, "K1s stages 16-byte slices");
     using SM = K1sSmem<LANES, VEC, WF, NC>;
@@ -157,6 +159,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 
     // Negatives of the current window, one per lane (lane q holds negative q).
     int negreg = (sub < n_neg && L >= 2) ? __ldg(negs + sub) : -1;
+    int tok_ahead = WF + 1 < L ? __ldg(ids + WF + 1) : -1;  // incoming position of window 0
     // Sample ids of the first chunk of the previous window (stale-prefetch check).
     int psid[NC];
 #pragma unroll
@@ -190,7 +193,15 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) vmask |= (tok[r] >= 0 ? 1u : 0u) << r;
         const int q_in = i + 1 + WF;
-        const int inc_tok = q_in < L ? __ldg(ids + q_in) : -1;
+        // Token ids run one window ahead of their rows, and the id/negative
+        // streams are pulled into L2 kPrefetchWindows ahead, so no row load
+        // waits on an id load that missed to DRAM.
+        const int inc_tok = tok_ahead;
+        tok_ahead = q_in + 1 < L ? __ldg(ids + q_in + 1) : -1;
+        if (sub == 0 && i + kPrefetchWindows < L) {
+            prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * n_neg);
+            prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
+        }
         float2 inc[H2];
         if (inc_tok >= 0) Row2<H2>::load(inc, syn0 + inc_tok * SM::STRIDE); else vzero2(inc);
         c_reads += inc_tok >= 0;
