@@ -93,6 +93,32 @@ struct Row2 {
     }
 };
 
+// Loads issued where they are written: asm volatile keeps the compiler from
+// sinking a prefetch-distance load down to its first use (which it otherwise
+// does to shorten live ranges, turning a one-window lookahead into none).
+__device__ __forceinline__ float4 ldcg_early(const float* p) {
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ldg_early(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+template <int H2>
+__device__ __forceinline__ void row_load_early(float2 (&v)[H2], const float* p) {
+    static_assert(H2 % 2 == 0, "16-byte slices");
+#pragma unroll
+    for (int i = 0; i < H2; i += 2) {
+        const float4 t = ldcg_early(p + 2 * i);
+        v[i] = make_float2(t.x, t.y);
+        v[i + 1] = make_float2(t.z, t.w);
+    }
+}
+
 template <int H2>
 __device__ __forceinline__ void vzero2(float2 (&v)[H2]) {
 #pragma unroll

@@ -197,15 +197,20 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         // streams are pulled into L2 kPrefetchWindows ahead, so no row load
         // waits on an id load that missed to DRAM.
         const int inc_tok = tok_ahead;
-        tok_ahead = q_in + 1 < L ? __ldg(ids + q_in + 1) : -1;
+        // Issued here, consumed at the end of the window (ring slide) and by the
+        // next window's prefetch: clamped addresses, no branches, no sinking.
+        float2 inc[H2];
+        row_load_early(inc, syn0 + max(inc_tok, 0) * SM::STRIDE);
+        const int last = max(L - 1, 0);
+        const int tok_raw = ldg_early(ids + min(q_in + 1, last));
+        const int neg_raw = n_neg > 0 ? ldg_early(negs + static_cast<size_t>(min(i + 1, last)) * n_neg + min(sub, n_neg - 1)) : -1;
+        tok_ahead = q_in + 1 < L ? tok_raw : -1;
+        const int negnext = (sub < n_neg && i + 1 < L) ? neg_raw : -1;
         if (sub == 0 && i + kPrefetchWindows < L) {
             prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * n_neg);
             prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
         }
-        float2 inc[H2];
-        if (inc_tok >= 0) Row2<H2>::load(inc, syn0 + inc_tok * SM::STRIDE); else vzero2(inc);
         c_reads += inc_tok >= 0;
-        const int negnext = (sub < n_neg && i + 1 < L) ? __ldg(negs + static_cast<size_t>(i + 1) * n_neg + sub) : -1;
         if constexpr (MULTI) {
 #pragma unroll
             for (int r = 0; r < NCTX; ++r) vzero2(dctx[r]);
