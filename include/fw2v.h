@@ -70,6 +70,9 @@ typedef struct fw2v_config {
     int32_t fast_sigmoid;  /* K1 sigmoid: 1 tanh.approx (|err| < 1e-3), 0 expf */
     int32_t k1_lanes;      /* 0 = auto; else lanes per sentence (4, 8, 16, 32) */
     int32_t streams;       /* 0 = workers; batching threads, one CUDA stream each */
+    int32_t l1_refresh_log2; /* K1s Hogwild sample reads: 0 = through L2 only (exact per-sentence
+                                order); k > 0 = through L1, each SM's L1 refreshed every 2^k windows
+                                (bounded staleness for Zipf-hot rows) */
 } fw2v_config;
 
 /* ringvec::TrafficCounters (traffic.hpp:19-40) plus totals. */

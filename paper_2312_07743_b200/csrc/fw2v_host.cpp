@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <ctime>
 #include <memory>
@@ -394,7 +395,8 @@ struct fw2v_ctx {
     std::vector<Lane> lanes;
     uint64_t words_trained = 0;  // schedule counter across calls (EmbeddingModel::words_trained)
 
-    ModelView model_view() const { return ModelView{syn0, syn1, cfg.dim, stride, vocab}; }
+    int32_t k1_flags = 0;
+    ModelView model_view() const { return ModelView{syn0, syn1, cfg.dim, stride, vocab, k1_flags}; }
 
     Sampler sampler() const {
         Sampler s;
@@ -539,6 +541,7 @@ void fw2v_config_default(fw2v_config* c) {
     c->fast_sigmoid = 1;
     c->k1_lanes = 0;
     c->streams = 0;
+    c->l1_refresh_log2 = 5;
 }
 
 int fw2v_validate_config(const fw2v_config* cfg) {
@@ -570,6 +573,12 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         }
         x->wf = context_width(x->cfg);
         x->vocab = vocab_size;
+        // Sample rows are always written as red.global.add of the window delta
+        // (row += delta, trainer.cpp:198-204); reads optionally go through L1.
+        x->k1_flags = kFlagRedSamples;
+        if (cfg->l1_refresh_log2 > 0)
+            x->k1_flags |= kFlagL1Samples | (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift);
+        if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments
         x->deterministic = cfg->deterministic == 1 || (cfg->deterministic < 0 && x->cfg.workers == 1);
         x->shape = choose_shape(cfg->dim, cfg->k1_lanes);
         x->stride = row_stride_for(cfg->dim, cfg->k1_lanes);

@@ -71,7 +71,19 @@ __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16_ca(float* smem, const float* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int H2>
+__device__ __forceinline__ void row_red_add(float* p, const float2 (&d)[H2]) {
+#pragma unroll
+    for (int i = 0; i < H2; i += 2)
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + 2 * i), "f"(d[i].x), "f"(d[i].y),
+                     "f"(d[i + 1].x), "f"(d[i + 1].y)
+                     : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 constexpr int kPrefetchWindows = 16;
 
@@ -179,10 +191,15 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             const int s = q == 0 ? target : nb;
             if (active && q <= n_neg && s >= 0) {
 #pragma unroll
-                for (int e = 0; e < VEC; e += 4) cp_async16(sbuf + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
+                for (int e = 0; e < VEC; e += 4) {
+                    if (m.flags & kFlagL1Samples) cp_async16_ca(sbuf + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
+                    else cp_async16(sbuf + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
+                }
             }
         }
     };
+    const int inval_log2 = (m.flags >> kFlagInvalShift) & 15;
+    const unsigned inval_mask = inval_log2 ? (1u << inval_log2) - 1u : 0u;
     if (!MULTI) prefetch(ttok, negreg, L >= 2);  // window 0's samples
     float2 dctx[MULTI ? NCTX : 1][H2];
 
@@ -314,8 +331,14 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
                     }
             }
             __syncwarp();
-            // Write back; a repeated id re-reads the row so both deltas land.
-            if (dup == 0) {
+            // Write back (row += delta). With kFlagRedSamples the delta is a
+            // vector reduction at L2 (exactly trainer.cpp:198-204, repeated ids
+            // included); otherwise a repeated id re-reads the row.
+            if (m.flags & kFlagRedSamples) {
+#pragma unroll
+                for (int q = 0; q < NC; ++q)
+                    if (sid[q] >= 0) row_red_add(syn1 + sid[q] * SM::STRIDE, D[q]);
+            } else if (dup == 0) {
 #pragma unroll
                 for (int q = 0; q < NC; ++q) {
 #pragma unroll
@@ -368,6 +391,11 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         vcopy2(ctx[NCTX - 1], inc);
         tok[NCTX - 1] = inc_tok;
         negreg = negnext;
+        // Bounded staleness for L1-cached sample rows: refresh this SM's L1.
+        if (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
+            (threadIdx.x >> 5) == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
     }
     // ContextRing::finish (trainer.cpp:71-75): residents in slot order.
     {
@@ -449,8 +477,11 @@ cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, 
     case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, ctr, st);
     case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, ctr, st);
     case 3: return launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, ctr, st);
-    case 4: return launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, ctr, st);
-    case 5: return launch_k1s_nc<LANES, VEC, 5, 4>(m, b, n_neg, fast, ctr, st);
+    // Wide windows: one 6-sample chunk when N+1 <= 6, else 4-sample chunks (registers).
+    case 4: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 4, 6>(m, b, n_neg, fast, ctr, st)
+                                  : launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, ctr, st);
+    case 5: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 5, 6>(m, b, n_neg, fast, ctr, st)
+                                  : launch_k1s_nc<LANES, VEC, 5, 4>(m, b, n_neg, fast, ctr, st);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -64,6 +64,7 @@ class CConfig(C.Structure):
         ("ignore_delimiters", C.c_int32),
         ("device", C.c_int32), ("deterministic", C.c_int32), ("sampler", C.c_int32),
         ("fast_sigmoid", C.c_int32), ("k1_lanes", C.c_int32), ("streams", C.c_int32),
+        ("l1_refresh_log2", C.c_int32),
     ]
 
 
@@ -121,6 +122,7 @@ class TrainConfig:
     fast_sigmoid: bool = True
     k1_lanes: int = 0
     streams: int = 0
+    l1_refresh_log2: int = 5
 
     @property
     def context_width(self) -> int:
