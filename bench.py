@@ -250,7 +250,7 @@ def run_ours(args, world, rank, local, dist):
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 e_rate = e_words * world / float(t.item())
             e2e = {"value": e_rate, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": 64 * cfg.streams * 1,
+                   "d2h_bytes_per_step": 64 * args.streams,
                    "path": "fw2v_train_corpus (C-ABI): host batching threads -> pinned -> H2D -> K1s"}
 
     peak, peak_src = load_peaks()
@@ -314,7 +314,7 @@ def cpu_baseline_leg(args, corpus):
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["text8", "1bw"], default="text8")
