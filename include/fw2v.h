@@ -73,6 +73,9 @@ typedef struct fw2v_config {
     int32_t l1_refresh_log2; /* K1s Hogwild sample reads: 0 = through L2 only (exact per-sentence
                                 order); k > 0 = through L1, each SM's L1 refreshed every 2^k windows
                                 (bounded staleness for Zipf-hot rows) */
+    int32_t delta_writeback; /* Hogwild kernels: 1 = rows leave the ring / sweep as red.add(final -
+                                loaded) so concurrent sentences never overwrite each other's updates;
+                                0 = overwrite, the reference's per-sentence write sequence exactly */
 } fw2v_config;
 
 /* ringvec::TrafficCounters (traffic.hpp:19-40) plus totals. */

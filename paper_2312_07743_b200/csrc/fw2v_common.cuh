@@ -131,6 +131,27 @@ __device__ __forceinline__ void vcopy2(float2 (&d)[H2], const float2 (&s)[H2]) {
     for (int i = 0; i < H2; ++i) d[i] = s[i];
 }
 
+// row += (v - v0) as a vector reduction at L2 (no lost updates under Hogwild).
+template <int VEC>
+__device__ __forceinline__ void red_add_delta(float* p, const float (&v)[VEC], const float (&v0)[VEC]) {
+    if constexpr (VEC % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + i), "f"(v[i] - v0[i]),
+                         "f"(v[i + 1] - v0[i + 1]), "f"(v[i + 2] - v0[i + 2]), "f"(v[i + 3] - v0[i + 3])
+                         : "memory");
+    } else if constexpr (VEC % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 2)
+            asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p + i), "f"(v[i] - v0[i]),
+                         "f"(v[i + 1] - v0[i + 1])
+                         : "memory");
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) atomicAdd(p + i, v[i] - v0[i]);
+    }
+}
+
 // Per-lane VEC-float slice of a row parked in shared memory.
 template <int VEC>
 __device__ __forceinline__ void stash_put(float* p, const float (&v)[VEC]) {

@@ -542,6 +542,7 @@ void fw2v_config_default(fw2v_config* c) {
     c->k1_lanes = 0;
     c->streams = 0;
     c->l1_refresh_log2 = 5;
+    c->delta_writeback = 1;
 }
 
 int fw2v_validate_config(const fw2v_config* cfg) {
@@ -575,7 +576,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         x->vocab = vocab_size;
         // Sample rows are always written as red.global.add of the window delta
         // (row += delta, trainer.cpp:198-204); reads optionally go through L1.
-        x->k1_flags = kFlagRedSamples;
+        x->k1_flags = kFlagRedSamples | (cfg->delta_writeback ? kFlagDeltaRing : 0);
         if (cfg->l1_refresh_log2 > 0)
             x->k1_flags |= kFlagL1Samples | (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift);
         if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments

@@ -64,7 +64,9 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
     // them in slot order; they are parked in shared memory until then.
     constexpr int C = NCTX + 1;
     extern __shared__ __align__(16) float k1_sh[];
-    float* stash = k1_sh + (threadIdx.x / LANES) * (C * LANES * VEC) + sub * VEC;
+    float* stash = k1_sh + (threadIdx.x / LANES) * (2 * C * LANES * VEC) + sub * VEC;
+    float* entry = stash + C * LANES * VEC;  // ring rows as loaded (delta write-back)
+    const bool delta_wb = (m.flags & kFlagDeltaRing) != 0;
     const int tail = L - C;
 
     // Window-relative ring: ctx[r] holds position i-WF+r (r < WF) or
@@ -74,11 +76,13 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
     float tgt[VEC];
     int ttok = L > 0 ? __ldg(ids) : -1;
     if (ttok >= 0) Row<VEC>::load(tgt, syn0 + ttok * stride); else vzero(tgt);
+    if (delta_wb) stash_put(entry, tgt);
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
         const int p = r - WF + 1;
         tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
         if (tok[r] >= 0) Row<VEC>::load(ctx[r], syn0 + tok[r] * stride); else vzero(ctx[r]);
+        if (delta_wb && r >= WF) stash_put(entry + p * (LANES * VEC), ctx[r]);
     }
     unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
     unsigned c_writes = 0, s_rw = 0, pairs = 0;
@@ -105,6 +109,8 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
             // The prefetch was issued before the previous sweep wrote its row
             // back: forward the register copy when both sweeps hit one row.
             if (sid != prev_sid) vcopy(s, nxt);
+            float s0[VEC];  // row as read, for the delta write-back
+            vcopy(s0, s);
             // Prefetch the next sweep's row: (i, k+1) or (i+1, 0).
             {
                 const bool same_win = k < n_neg;
@@ -132,7 +138,10 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
                 }
                 pairs += valid;
             }
-            if (wact) Row<VEC>::store(syn1 + sid * stride, s);
+            if (wact) {
+                if (delta_wb) red_add_delta(syn1 + sid * stride, s, s0);
+                else Row<VEC>::store(syn1 + sid * stride, s);
+            }
             s_rw += wact;
             prev_sid = wact ? sid : -1;
         }
@@ -141,11 +150,19 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
         const int etok = tok[0];
         if (etok >= 0) {
             const int p = i - WF;
-            if (p >= tail) stash_put(stash + (p % C) * (LANES * VEC), ctx[0]);
-            else Row<VEC>::store(syn0 + etok * stride, ctx[0]);
+            if (delta_wb) {
+                float e0[VEC];
+                stash_get(e0, entry + (p % C) * (LANES * VEC));
+                red_add_delta(syn0 + etok * stride, ctx[0], e0);
+            } else if (p >= tail) {
+                stash_put(stash + (p % C) * (LANES * VEC), ctx[0]);
+            } else {
+                Row<VEC>::store(syn0 + etok * stride, ctx[0]);
+            }
             ++c_writes;
             if (inc_tok == etok) vcopy(inc, ctx[0]);  // load-after-evict forwarding
         }
+        if (delta_wb && inc_tok >= 0) stash_put(entry + ((i + 1 + WF) % C) * (LANES * VEC), inc);
 #pragma unroll
         for (int r = 0; r < WF - 1; ++r) { vcopy(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
         vcopy(ctx[WF - 1], tgt);
@@ -157,14 +174,33 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
         vcopy(ctx[NCTX - 1], inc);
         tok[NCTX - 1] = inc_tok;
     }
-    // ContextRing::finish (trainer.cpp:71-75): residents written in slot order.
+    // ContextRing::finish (trainer.cpp:71-75): residents written in slot order
+    // (deltas commute, so delta write-back needs no ordering).
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
         const int p = r < WF ? Lmax - WF + r : Lmax + 1 + (r - WF);
-        if (tok[r] >= 0) { stash_put(stash + (p % C) * (LANES * VEC), ctx[r]); ++c_writes; }
+        if (tok[r] >= 0) {
+            if (delta_wb) {
+                float e0[VEC];
+                stash_get(e0, entry + (p % C) * (LANES * VEC));
+                red_add_delta(syn0 + tok[r] * stride, ctx[r], e0);
+            } else {
+                stash_put(stash + (p % C) * (LANES * VEC), ctx[r]);
+            }
+            ++c_writes;
+        }
     }
-    if (ttok >= 0) { stash_put(stash + (Lmax % C) * (LANES * VEC), tgt); ++c_writes; }
-    {
+    if (ttok >= 0) {
+        if (delta_wb) {
+            float e0[VEC];
+            stash_get(e0, entry + (Lmax % C) * (LANES * VEC));
+            red_add_delta(syn0 + ttok * stride, tgt, e0);
+        } else {
+            stash_put(stash + (Lmax % C) * (LANES * VEC), tgt);
+        }
+        ++c_writes;
+    }
+    if (!delta_wb) {
         const int first = max(0, tail);
         for (int s = 0; s < C; ++s) {
             const int p = first + ((s - first % C) + C) % C;
@@ -504,7 +540,7 @@ cudaError_t launch_k1_wf(const ModelView& m, const BatchView& b, int n_neg, bool
     const int warps = (b.n_sentences + GPW - 1) / GPW;
     const int blocks = (warps * 32 + kK1Threads - 1) / kK1Threads;
     if (blocks == 0) return cudaSuccess;
-    constexpr int bytes = kK1Threads * (2 * WF + 1) * VEC * 4;  // finish stash per lane group
+    constexpr int bytes = 2 * kK1Threads * (2 * WF + 1) * VEC * 4;  // finish stash + ring entry values
     auto* kern = fast ? k1_lifetime<LANES, VEC, WF, true> : k1_lifetime<LANES, VEC, WF, false>;
     if (bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);

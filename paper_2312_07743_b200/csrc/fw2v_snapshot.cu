@@ -84,6 +84,15 @@ __device__ __forceinline__ void row_red_add(float* p, const float2 (&d)[H2]) {
                      "f"(d[i + 1].x), "f"(d[i + 1].y)
                      : "memory");
 }
+// red.add(value - entry_value): the ring row's accumulated update since it was loaded.
+template <int H2>
+__device__ __forceinline__ void row_red_delta(float* p, const float2 (&v)[H2], const float* entry_smem) {
+    float2 e[H2];
+    Row2<H2>::load_shared(e, entry_smem);
+#pragma unroll
+    for (int i = 0; i < H2; ++i) e[i] = make_float2(v[i].x - e[i].x, v[i].y - e[i].y);
+    row_red_add(p, e);
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 constexpr int kPrefetchWindows = 16;
 
@@ -94,7 +103,8 @@ struct K1sSmem {
     static constexpr int NV = NC * NCTX;
     static constexpr int STRIDE = LANES * VEC;
     // per group: g pairs, sample prefetch buffer, finish stash
-    static constexpr int kGroupFloats = 2 * NV + NC * STRIDE + C * STRIDE;
+    // per group: g pairs, sample prefetch buffer, finish stash, ring entry values
+    static constexpr int kGroupFloats = 2 * NV + NC * STRIDE + 2 * C * STRIDE;
     static constexpr int kBlockBytes = (kK1Threads / LANES) * kGroupFloats * 4;
 };
 
@@ -122,6 +132,9 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     float2* g2 = reinterpret_cast<float2*>(gsh);
     float* sbuf = gsh + 2 * NV + sub * VEC;                     // + q*STRIDE
     float* stash = gsh + 2 * NV + NC * SM::STRIDE + sub * VEC;  // + slot*STRIDE
+    // Ring rows as loaded (delta write-back: red.add(final - loaded)).
+    float* entry = gsh + 2 * NV + (NC + C) * SM::STRIDE + sub * VEC;
+    const bool delta_wb = (m.flags & kFlagDeltaRing) != 0;
 
     uint32_t beg = 0, len = 0;
     float alpha = 0.0f;
@@ -160,11 +173,13 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     float2 tgt[H2];
     int ttok = L > 0 ? __ldg(ids) : -1;
     if (ttok >= 0) Row2<H2>::load(tgt, syn0 + ttok * SM::STRIDE); else vzero2(tgt);
+    if (delta_wb) Row2<H2>::store_shared(entry, tgt);  // position 0 -> slot 0
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
         const int p = r - WF + 1;
         tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
         if (tok[r] >= 0) Row2<H2>::load(ctx[r], syn0 + tok[r] * SM::STRIDE); else vzero2(ctx[r]);
+        if (delta_wb && r >= WF) Row2<H2>::store_shared(entry + p * SM::STRIDE, ctx[r]);  // p < C
     }
     unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
     unsigned s_rw = 0, pairs = 0;
@@ -376,10 +391,16 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         const int etok = tok[0];
         if (etok >= 0) {
             const int p = i - WF;
-            if (p >= tail) Row2<H2>::store_shared(stash + (p % C) * SM::STRIDE, ctx[0]);
-            else Row2<H2>::store(syn0 + etok * SM::STRIDE, ctx[0]);
+            if (delta_wb) {
+                row_red_delta(syn0 + etok * SM::STRIDE, ctx[0], entry + (p % C) * SM::STRIDE);
+            } else if (p >= tail) {
+                Row2<H2>::store_shared(stash + (p % C) * SM::STRIDE, ctx[0]);
+            } else {
+                Row2<H2>::store(syn0 + etok * SM::STRIDE, ctx[0]);
+            }
             if (inc_tok == etok) vcopy2(inc, ctx[0]);
         }
+        if (delta_wb && inc_tok >= 0) Row2<H2>::store_shared(entry + (q_in % C) * SM::STRIDE, inc);
 #pragma unroll
         for (int r = 0; r < WF - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
         vcopy2(ctx[WF - 1], tgt);
@@ -398,7 +419,16 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         }
     }
     // ContextRing::finish (trainer.cpp:71-75): residents in slot order.
-    {
+    if (delta_wb) {
+        // Deltas commute: no ordering to preserve.
+        const int i_end = Lmax;
+#pragma unroll
+        for (int r = 0; r < NCTX; ++r) {
+            const int p = r < WF ? i_end - WF + r : i_end + 1 + (r - WF);
+            if (tok[r] >= 0) row_red_delta(syn0 + tok[r] * SM::STRIDE, ctx[r], entry + (p % C) * SM::STRIDE);
+        }
+        if (ttok >= 0) row_red_delta(syn0 + ttok * SM::STRIDE, tgt, entry + (i_end % C) * SM::STRIDE);
+    } else {
         const int i_end = Lmax;  // registers hold positions i_end-WF .. i_end+WF
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) {

@@ -83,7 +83,7 @@ def test_k1_single_sentence_semantics(oracle, dim, lanes, window, mode):
     negs = fixed_negatives(int(offsets[-1]), n_neg, V, seed=9)
     alphas = np.full(len(offsets) - 1, 0.025, np.float32)
     cfg = dict(dim=dim, window=window, negatives=n_neg, workers=4, reuse_mode=mode)
-    gcfg = dict(cfg, deterministic=0, fast_sigmoid=False, k1_lanes=lanes, l1_refresh_log2=0)
+    gcfg = dict(cfg, deterministic=0, fast_sigmoid=False, k1_lanes=lanes, l1_refresh_log2=0, delta_writeback=False)
     ri, _ = oracle.init_model(V, dim, 5)
     ro = (ri[::-1] * 4.0).copy()
     gi0, go0 = ri.copy(), ro.copy()
