@@ -185,7 +185,15 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     unsigned s_rw = 0, pairs = 0;
 
     // Negatives of the current window, one per lane (lane q holds negative q).
-    int negreg = (sub < n_neg && L >= 2) ? __ldg(negs + sub) : -1;
+    // Negatives of a window, two per lane: lane q holds negative q (negreg.x)
+    // and negative q + LANES (negreg.y), so N <= 2 * LANES.
+    int2 negreg = make_int2((sub < n_neg && L >= 2) ? __ldg(negs + sub) : -1,
+                            (sub + LANES < n_neg && L >= 2) ? __ldg(negs + sub + LANES) : -1);
+    // Negative j (0-based) of the window held in `nr`, broadcast within the group.
+    auto neg_of = [&](int2 nr, int j) {
+        const int v = __shfl_sync(kFull, j < LANES ? nr.x : nr.y, j & (LANES - 1), LANES);
+        return v;
+    };
     int tok_ahead = WF + 1 < L ? __ldg(ids + WF + 1) : -1;  // incoming position of window 0
     // Sample ids of the first chunk of the previous window (stale-prefetch check).
     int psid[NC];
@@ -199,10 +207,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 #pragma unroll
             for (int e = 0; e < VEC; e += 4) *reinterpret_cast<float4*>(sbuf + q * SM::STRIDE + e) = z;
     }
-    auto prefetch = [&](int target, int negv, bool active) {
+    auto prefetch = [&](int target, int2 negv, bool active) {
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-            const int nb = __shfl_sync(kFull, negv, (q + LANES - 1) & (LANES - 1), LANES);
+            const int nb = neg_of(negv, q > 0 ? q - 1 : 0);
             const int s = q == 0 ? target : nb;
             if (active && q <= n_neg && s >= 0) {
 #pragma unroll
@@ -235,9 +243,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         row_load_early(inc, syn0 + max(inc_tok, 0) * SM::STRIDE);
         const int last = max(L - 1, 0);
         const int tok_raw = ldg_early(ids + min(q_in + 1, last));
-        const int neg_raw = n_neg > 0 ? ldg_early(negs + static_cast<size_t>(min(i + 1, last)) * n_neg + min(sub, n_neg - 1)) : -1;
+        const int* nrow = negs + static_cast<size_t>(min(i + 1, last)) * n_neg;
+        const int neg_raw = n_neg > 0 ? ldg_early(nrow + min(sub, n_neg - 1)) : -1;
+        const int neg_raw2 = n_neg > LANES ? ldg_early(nrow + min(sub + LANES, n_neg - 1)) : -1;
         tok_ahead = q_in + 1 < L ? tok_raw : -1;
-        const int negnext = (sub < n_neg && i + 1 < L) ? neg_raw : -1;
+        const int2 negnext = make_int2((sub < n_neg && i + 1 < L) ? neg_raw : -1,
+                                       (sub + LANES < n_neg && i + 1 < L) ? neg_raw2 : -1);
         if (sub == 0 && i + kPrefetchWindows < L) {
             prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * n_neg);
             prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
@@ -256,8 +267,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 #pragma unroll
             for (int q = 0; q < NC; ++q) {
                 const int kk = kbase + q;
-                const int src = MULTI ? ((kk - 1) & (LANES - 1)) : ((q + LANES - 1) & (LANES - 1));
-                const int nb = __shfl_sync(kFull, negreg, src, LANES);
+                const int nb = neg_of(negreg, kk > 0 ? kk - 1 : 0);
                 const int s = kk == 0 ? ttok : nb;
                 sid[q] = (wact && kk <= n_neg) ? s : -1 - q;  // empty slots: distinct negative ids
             }
@@ -516,9 +526,9 @@ cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, 
     }
 }
 
-#define FW2V_K1S_SHAPES(X) X(16, 4) X(32, 4) X(32, 8)
+#define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(32, 4) X(32, 8)
 
-// Requires n_neg <= LANES (negatives are distributed one per lane).
+// Requires n_neg <= 2 * LANES (negatives are distributed two per lane).
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
                        DevCounters* ctr, cudaStream_t st) {
 #define FW2V_CASE(L_, V_) \
@@ -529,7 +539,7 @@ cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& 
 }
 
 bool k1s_supported(int lanes, int vec, int n_neg, int wf) {
-    if (n_neg > lanes || wf < 1 || wf > 5) return false;
+    if (n_neg > 2 * lanes || wf < 1 || wf > 5) return false;
 #define FW2V_CASE(L_, V_) if (lanes == L_ && vec == V_) return true;
     FW2V_K1S_SHAPES(FW2V_CASE)
 #undef FW2V_CASE

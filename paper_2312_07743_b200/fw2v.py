@@ -268,7 +268,9 @@ class Corpus:
     def head(self, n_sentences: int) -> "Corpus":
         """First n sentences (a bounded sample for CPU baselines); same vocabulary."""
         off = np.ascontiguousarray(self.offsets[: n_sentences + 1])
-        return Corpus(self.counts, off, self.ids[: int(off[-1])])
+        c = Corpus(self.counts, off, self.ids[: int(off[-1])])
+        c._parent = self  # the views borrow this corpus's C buffers
+        return c
 
 
 def synth_zipf(types, tokens, s=1.0, sentence_len=1000, min_count=5, threads=0) -> Corpus:
