@@ -17,10 +17,10 @@ pytestmark = pytest.mark.gpu
 fw = pytest.importorskip("paper_2312_07743_b200")
 from oracle.oracle import TrainConfig as RConfig  # noqa: E402
 
-TOPICS, PER_TOPIC, SHARED = 100, 20, 100
+TOPICS, PER_TOPIC, SHARED = 500, 20, 500
 
 
-def planted_corpus(n_sentences=12000, length=30, seed=20240811):
+def planted_corpus(n_sentences=100_000, length=30, seed=20240811):
     """Returns counts (true frequencies, vocabulary order), offsets, ids and the
     topic of every vocabulary id (-1 for shared words)."""
     rng = np.random.default_rng(seed)
@@ -54,7 +54,7 @@ def recall_at_10(inp, word_topic):
     return float(same.mean())
 
 
-CFG = dict(dim=32, window=5, negatives=5, epochs=5, batch_sentences=500, subsample=1e-3, table_size=1_000_003,
+CFG = dict(dim=32, window=5, negatives=5, epochs=3, batch_sentences=1000, subsample=1e-3, table_size=1_000_003,
            alpha0=0.025, seed=3)
 
 
