@@ -296,11 +296,6 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 #pragma unroll
                 for (int q = 0; q < NC; ++q) Row2<H2>::load(S[q], syn1 + max(sid[q], 0) * SM::STRIDE);
             }
-            unsigned dup = 0;
-#pragma unroll
-            for (int q = 1; q < NC; ++q)
-#pragma unroll
-                for (int j = 0; j < q; ++j) dup |= (sid[q] == sid[j] ? 1u : 0u) << q;
 
             // 1-2. all dots of the chunk, then one transposed butterfly.
             float P[NV];
@@ -356,31 +351,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
                     }
             }
             __syncwarp();
-            // Write back (row += delta). With kFlagRedSamples the delta is a
-            // vector reduction at L2 (exactly trainer.cpp:198-204, repeated ids
-            // included); otherwise a repeated id re-reads the row.
-            if (m.flags & kFlagRedSamples) {
+            // Write back (row += delta) as a vector reduction at L2: exactly
+            // trainer.cpp:198-204 (repeated ids included), and no read-modify-
+            // write round trip on Zipf-hot rows.
 #pragma unroll
-                for (int q = 0; q < NC; ++q)
-                    if (sid[q] >= 0) row_red_add(syn1 + sid[q] * SM::STRIDE, D[q]);
-            } else if (dup == 0) {
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-#pragma unroll
-                    for (int h = 0; h < H2; ++h) S[q][h] = __fadd2_rn(S[q][h], D[q][h]);
-                    if (sid[q] >= 0) Row2<H2>::store(syn1 + sid[q] * SM::STRIDE, S[q]);
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    if (sid[q] < 0) continue;
-                    float* row = syn1 + sid[q] * SM::STRIDE;
-                    if ((dup >> q) & 1u) Row2<H2>::load(S[q], row);
-#pragma unroll
-                    for (int h = 0; h < H2; ++h) S[q][h] = __fadd2_rn(S[q][h], D[q][h]);
-                    Row2<H2>::store(row, S[q]);
-                }
-            }
+            for (int q = 0; q < NC; ++q)
+                if (sid[q] >= 0) row_red_add(syn1 + sid[q] * SM::STRIDE, D[q]);
             if (ch == 0) {
 #pragma unroll
                 for (int q = 0; q < NC; ++q) psid[q] = sid[q] >= 0 ? sid[q] : -100;
