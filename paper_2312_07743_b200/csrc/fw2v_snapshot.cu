@@ -104,7 +104,8 @@ struct K1sSmem {
     static constexpr int STRIDE = LANES * VEC;
     // per group: g pairs, sample prefetch buffer, finish stash
     // per group: g pairs, sample prefetch buffer, finish stash, ring entry values
-    static constexpr int kGroupFloats = 2 * NV + NC * STRIDE + 2 * C * STRIDE;
+    // (sample buffers are double-buffered by window parity)
+    static constexpr int kGroupFloats = 2 * NV + 2 * NC * STRIDE + 2 * C * STRIDE;
     static constexpr int kBlockBytes = (kK1Threads / LANES) * kGroupFloats * 4;
 };
 
@@ -130,10 +131,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     const bool has = sent < b.n_sentences;
     float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
     float2* g2 = reinterpret_cast<float2*>(gsh);
-    float* sbuf = gsh + 2 * NV + sub * VEC;                     // + q*STRIDE
-    float* stash = gsh + 2 * NV + NC * SM::STRIDE + sub * VEC;  // + slot*STRIDE
+    float* sbuf = gsh + 2 * NV + sub * VEC;                         // + (parity*NC + q)*STRIDE
+    float* stash = gsh + 2 * NV + 2 * NC * SM::STRIDE + sub * VEC;  // + slot*STRIDE
     // Ring rows as loaded (delta write-back: red.add(final - loaded)).
-    float* entry = gsh + 2 * NV + (NC + C) * SM::STRIDE + sub * VEC;
+    float* entry = gsh + 2 * NV + (2 * NC + C) * SM::STRIDE + sub * VEC;
     const bool delta_wb = (m.flags & kFlagDeltaRing) != 0;
 
     uint32_t beg = 0, len = 0;
@@ -203,11 +204,13 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     {
         const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
-        for (int q = 0; q < NC; ++q)
+        for (int q = 0; q < 2 * NC; ++q)
 #pragma unroll
             for (int e = 0; e < VEC; e += 4) *reinterpret_cast<float4*>(sbuf + q * SM::STRIDE + e) = z;
     }
-    auto prefetch = [&](int target, int2 negv, bool active) {
+    const bool l1_samples = (m.flags & kFlagL1Samples) != 0;
+    auto prefetch = [&](int target, int2 negv, bool active, int parity) {
+        float* dst = sbuf + parity * NC * SM::STRIDE;
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
             const int nb = neg_of(negv, q > 0 ? q - 1 : 0);
@@ -215,15 +218,19 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             if (active && q <= n_neg && s >= 0) {
 #pragma unroll
                 for (int e = 0; e < VEC; e += 4) {
-                    if (m.flags & kFlagL1Samples) cp_async16_ca(sbuf + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
-                    else cp_async16(sbuf + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
+                    if (l1_samples) cp_async16_ca(dst + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
+                    else cp_async16(dst + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
                 }
             }
         }
     };
     const int inval_log2 = (m.flags >> kFlagInvalShift) & 15;
     const unsigned inval_mask = inval_log2 ? (1u << inval_log2) - 1u : 0u;
-    if (!MULTI) prefetch(ttok, negreg, L >= 2);  // window 0's samples
+    // Negatives of the next window (window i+1 while window i runs): the
+    // prefetch of window i+1's rows is issued at the start of window i.
+    int2 negnext = make_int2((sub < n_neg && L >= 2) ? __ldg(negs + n_neg + sub) : -1,
+                             (sub + LANES < n_neg && L >= 2) ? __ldg(negs + n_neg + sub + LANES) : -1);
+    if (!MULTI) prefetch(ttok, negreg, L >= 2, 0);  // window 0's samples
     float2 dctx[MULTI ? NCTX : 1][H2];
 
     for (int i = 0; i < Lmax; ++i) {
@@ -243,12 +250,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         row_load_early(inc, syn0 + max(inc_tok, 0) * SM::STRIDE);
         const int last = max(L - 1, 0);
         const int tok_raw = ldg_early(ids + min(q_in + 1, last));
-        const int* nrow = negs + static_cast<size_t>(min(i + 1, last)) * n_neg;
+        const int* nrow = negs + static_cast<size_t>(min(i + 2, last)) * n_neg;
         const int neg_raw = n_neg > 0 ? ldg_early(nrow + min(sub, n_neg - 1)) : -1;
         const int neg_raw2 = n_neg > LANES ? ldg_early(nrow + min(sub + LANES, n_neg - 1)) : -1;
         tok_ahead = q_in + 1 < L ? tok_raw : -1;
-        const int2 negnext = make_int2((sub < n_neg && i + 1 < L) ? neg_raw : -1,
-                                       (sub + LANES < n_neg && i + 1 < L) ? neg_raw2 : -1);
+        const int2 negnext2 = make_int2((sub < n_neg && i + 2 < L) ? neg_raw : -1,
+                                        (sub + LANES < n_neg && i + 2 < L) ? neg_raw2 : -1);
         if (sub == 0 && i + kPrefetchWindows < L) {
             prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * n_neg);
             prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
@@ -277,7 +284,9 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
                 // window rewrote after the prefetch was issued are re-read.
                 cp_async_wait_all();
 #pragma unroll
-                for (int q = 0; q < NC; ++q) Row2<H2>::load_shared(S[q], sbuf + q * SM::STRIDE);
+                for (int q = 0; q < NC; ++q) Row2<H2>::load_shared(S[q], sbuf + ((i & 1) * NC + q) * SM::STRIDE);
+                // Next window's rows go to the other buffer right away.
+                if (i + 1 < Lmax) prefetch(tok[WF], negnext, i + 1 < L && L >= 2, (i + 1) & 1);
                 bool stale = false;
 #pragma unroll
                 for (int q = 0; q < NC; ++q)
@@ -310,8 +319,6 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
                 }
             BF::reduce(P, sub);
 
-            // Next window's first chunk: its ids have arrived by now.
-            if (!MULTI && i + 1 < Lmax) prefetch(tok[WF], negnext, i + 1 < L && L >= 2);
 
             // 3. sigmoid on owned slots, publish g pairs.
 #pragma unroll
@@ -398,6 +405,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         vcopy2(ctx[NCTX - 1], inc);
         tok[NCTX - 1] = inc_tok;
         negreg = negnext;
+        negnext = negnext2;
         // Bounded staleness for L1-cached sample rows: refresh this SM's L1.
         if (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
             (threadIdx.x >> 5) == 0) {
