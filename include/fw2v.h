@@ -76,6 +76,9 @@ typedef struct fw2v_config {
     int32_t delta_writeback; /* Hogwild kernels: 1 = rows leave the ring / sweep as red.add(final -
                                 loaded) so concurrent sentences never overwrite each other's updates;
                                 0 = overwrite, the reference's per-sentence write sequence exactly */
+    int32_t max_inflight;  /* Hogwild: sentences in flight on the device at once, summed over the
+                              streams. 0 = auto (collision budget from the vocabulary, see DESIGN.md
+                              §5), -1 = unlimited (every sentence of a batch in one launch) */
 } fw2v_config;
 
 /* ringvec::TrafficCounters (traffic.hpp:19-40) plus totals. */

@@ -34,14 +34,15 @@
 #include "fw2v_device.cuh"
 
 namespace fw2v {
+// resident != nullptr: no launch; *resident = sentences of that kernel the device holds at once.
 cudaError_t launch_k1(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf,
-                      bool fast, DevCounters* ctr, cudaStream_t st);
+                      bool fast, DevCounters* ctr, cudaStream_t st, int* resident = nullptr);
 bool k1_shape_supported(int lanes, int vec);
 cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf, int mode, bool serial,
                       DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st);
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
-                       DevCounters* ctr, cudaStream_t st);
+                       DevCounters* ctr, cudaStream_t st, int* resident = nullptr);
 bool k1s_supported(int lanes, int vec, int n_neg, int wf);
 } // namespace fw2v
 
@@ -396,6 +397,7 @@ struct fw2v_ctx {
     uint64_t words_trained = 0;  // schedule counter across calls (EmbeddingModel::words_trained)
 
     int32_t k1_flags = 0;
+    int64_t inflight_total = 0;  // Hogwild sentences in flight over all streams (0 = unlimited)
     ModelView model_view() const { return ModelView{syn0, syn1, cfg.dim, stride, vocab, k1_flags}; }
 
     Sampler sampler() const {
@@ -421,14 +423,44 @@ struct fw2v_ctx {
         return p;
     }
 
-    cudaError_t launch(const BatchView& bv, bool serial, DevCounters* ctr, cudaStream_t st) const {
+    // Hogwild sentences in flight per stream (0 = no cap): a batch larger than
+    // the cap runs as consecutive launches on its stream.
+    int64_t inflight_per_stream(int streams) const {
+        if (inflight_total <= 0) return 0;
+        return std::max<int64_t>(1, inflight_total / std::max(1, streams));
+    }
+
+    cudaError_t launch(const BatchView& bv, bool serial, DevCounters* ctr, cudaStream_t st, int streams = 1) const {
+        const int64_t cap = serial ? 0 : inflight_per_stream(streams);
+        if (cap > 0 && bv.n_sentences > cap) {
+            for (int64_t s0 = 0; s0 < bv.n_sentences; s0 += cap) {
+                BatchView sub = bv;
+                sub.offsets = bv.offsets + s0;
+                sub.alpha = bv.alpha + s0;
+                sub.n_sentences = static_cast<int32_t>(std::min<int64_t>(cap, bv.n_sentences - s0));
+                cudaError_t e = launch_one(sub, false, ctr, st);
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
+        return launch_one(bv, serial, ctr, st);
+    }
+
+    // resident != nullptr: no launch, *resident = sentences the Hogwild kernel
+    // holds on the device at once (0 when unknown).
+    cudaError_t launch_one(const BatchView& bv, bool serial, DevCounters* ctr, cudaStream_t st,
+                           int* resident = nullptr) const {
         const ModelView mv = model_view();
-        if (serial) return launch_k2(mv, bv, cfg.negatives, wf, cfg.reuse_mode, true, ctr, st);
-        if (cfg.reuse_mode == kLifetime && shape.lanes > 0 && wf <= 5)
-            return launch_k1(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, cfg.fast_sigmoid != 0, ctr, st);
-        if (cfg.reuse_mode == kWindowSnapshot && k1s_supported(shape.lanes, shape.vec, cfg.negatives, wf))
-            return launch_k1s(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, cfg.fast_sigmoid != 0, ctr, st);
-        return launch_k2(mv, bv, cfg.negatives, wf, cfg.reuse_mode, false, ctr, st);
+        const bool fast = cfg.fast_sigmoid != 0;
+        if (!serial && cfg.reuse_mode == kLifetime && shape.lanes > 0 && wf <= 5)
+            return launch_k1(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, fast, ctr, st, resident);
+        if (!serial && cfg.reuse_mode == kWindowSnapshot && k1s_supported(shape.lanes, shape.vec, cfg.negatives, wf))
+            return launch_k1s(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, fast, ctr, st, resident);
+        if (resident != nullptr) {
+            *resident = 0;
+            return cudaSuccess;
+        }
+        return launch_k2(mv, bv, cfg.negatives, wf, cfg.reuse_mode, serial, ctr, st);
     }
 
     void ensure_lanes(int n, uint64_t cap_words, uint64_t cap_sent) {
@@ -509,6 +541,25 @@ uint64_t expected_epoch_words(const fw2v_ctx& x) {  // trainer.cpp:378-386
     return r > 0 ? r : 1;
 }
 
+// Hogwild collision budget. A sample row is drawn with
+// probability p_w ~ count^power; with M sentences in flight, a drawn row is
+// being updated by ~M (N+1) sum_w p_w^2 = M (N+1) / V_eff other sentences at
+// the same time, and their summed deltas act as one step of that many times
+// alpha. Capping M at 2 V_eff keeps that factor near the reference's (a few
+// CPU threads) on tiny vocabularies, and never binds on real ones (text8:
+// V_eff = 1,472 -> 2,944; 1bw: 8,572; both above the ~1,800 sentences the
+// GPU holds resident).
+int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power) {
+    double z = 0.0, z2 = 0.0;
+    for (int32_t w = 0; w < vocab_size; ++w) {
+        const double p = std::pow(static_cast<double>(counts[w]), power);
+        z += p;
+        z2 += p * p;
+    }
+    const double v_eff = z2 > 0.0 ? z * z / z2 : 1.0;
+    return std::max<int64_t>(32, static_cast<int64_t>(std::ceil(2.0 * v_eff)));
+}
+
 } // namespace
 
 extern "C" {
@@ -543,6 +594,7 @@ void fw2v_config_default(fw2v_config* c) {
     c->streams = 0;
     c->l1_refresh_log2 = 5;
     c->delta_writeback = 1;
+    c->max_inflight = 0;
 }
 
 int fw2v_validate_config(const fw2v_config* cfg) {
@@ -580,6 +632,8 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         if (cfg->l1_refresh_log2 > 0)
             x->k1_flags |= kFlagL1Samples | (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift);
         if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments
+        x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
+                            : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power) : 0;
         x->deterministic = cfg->deterministic == 1 || (cfg->deterministic < 0 && x->cfg.workers == 1);
         x->shape = choose_shape(cfg->dim, cfg->k1_lanes);
         x->stride = row_stride_for(cfg->dim, cfg->k1_lanes);
@@ -600,6 +654,12 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         Rng r = Rng::derive(cfg->seed, 0x696e6974ULL);  // "init" stream, model.cpp:26
         FW2V_CK(launch_init_model(x->model_view(), r.state, nullptr));
         FW2V_CK(cudaDeviceSynchronize());
+        if (x->inflight_total > 0 && !x->deterministic) {
+            // The budget only matters when it is below what the device holds at once.
+            int resident = 0;
+            FW2V_CK(x->launch_one(BatchView{}, false, nullptr, nullptr, &resident));
+            if (cfg->max_inflight == 0 && resident > 0 && resident <= x->inflight_total) x->inflight_total = 0;
+        }
         *out = x.release();
     });
 }
@@ -689,7 +749,7 @@ int fw2v_train_sentences(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_senten
         FW2V_CK(cudaMalloc(&d_ctr, sizeof(DevCounters))); guard.p[4] = d_ctr;
         FW2V_CK(cudaMemset(d_ctr, 0, sizeof(DevCounters)));
         if (words) FW2V_CK(cudaMemcpy(d_ids, ids + offsets[0], 4 * words, cudaMemcpyHostToDevice));
-        if (words * n) FW2V_CK(cudaMemcpy(d_negs, negatives, 4 * words * n, cudaMemcpyHostToDevice));
+        if (words != 0 && n != 0) FW2V_CK(cudaMemcpy(d_negs, negatives, 4 * words * n, cudaMemcpyHostToDevice));
         FW2V_CK(cudaMemcpy(d_off, off.data(), 4 * (n_sentences + 1), cudaMemcpyHostToDevice));
         if (n_sentences) FW2V_CK(cudaMemcpy(d_alpha, alphas, 4 * n_sentences, cudaMemcpyHostToDevice));
         BatchView bv{d_ids, d_off, d_negs, d_alpha, static_cast<int32_t>(n_sentences)};
@@ -795,7 +855,7 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                             sl.in_flight = true;
                             h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
                             const BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
-                            FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st));
+                            FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, P));
                             which ^= 1;
                         }
                         batch_words.fetch_add(wsum);
@@ -963,7 +1023,7 @@ int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* 
             for (int p = 0; p < P; ++p)
                 if (k < plan->lanes[static_cast<size_t>(p)].size())
                     FW2V_CK(x->launch(plan->lanes[static_cast<size_t>(p)][k].view, x->deterministic,
-                                      x->lanes[static_cast<size_t>(p)].d_ctr, x->lanes[static_cast<size_t>(p)].stream));
+                                      x->lanes[static_cast<size_t>(p)].d_ctr, x->lanes[static_cast<size_t>(p)].stream, P));
         for (int p = 0; p < P; ++p) FW2V_CK(cudaEventRecord(ends[static_cast<size_t>(p)], x->lanes[static_cast<size_t>(p)].stream));
         float ms_max = 0.0f;
         for (int p = 0; p < P; ++p) {

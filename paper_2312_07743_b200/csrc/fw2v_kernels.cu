@@ -535,30 +535,31 @@ struct K1Shape {
 
 template <int LANES, int VEC, int WF>
 cudaError_t launch_k1_wf(const ModelView& m, const BatchView& b, int n_neg, bool fast,
-                         DevCounters* ctr, cudaStream_t st) {
+                         DevCounters* ctr, cudaStream_t st, int* resident) {
     constexpr int GPW = 32 / LANES;
     const int warps = (b.n_sentences + GPW - 1) / GPW;
     const int blocks = (warps * 32 + kK1Threads - 1) / kK1Threads;
-    if (blocks == 0) return cudaSuccess;
     constexpr int bytes = 2 * kK1Threads * (2 * WF + 1) * VEC * 4;  // finish stash + ring entry values
     auto* kern = fast ? k1_lifetime<LANES, VEC, WF, true> : k1_lifetime<LANES, VEC, WF, false>;
     if (bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         if (e != cudaSuccess) return e;
     }
+    if (resident != nullptr) return resident_sentences(kern, bytes, kK1Threads / LANES, resident);
+    if (blocks == 0) return cudaSuccess;
     kern<<<blocks, kK1Threads, bytes, st>>>(m, b, n_neg, ctr);
     return cudaGetLastError();
 }
 
 template <int LANES, int VEC>
 cudaError_t launch_k1_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
-                            DevCounters* ctr, cudaStream_t st) {
+                            DevCounters* ctr, cudaStream_t st, int* resident) {
     switch (wf) {
-    case 1: return launch_k1_wf<LANES, VEC, 1>(m, b, n_neg, fast, ctr, st);
-    case 2: return launch_k1_wf<LANES, VEC, 2>(m, b, n_neg, fast, ctr, st);
-    case 3: return launch_k1_wf<LANES, VEC, 3>(m, b, n_neg, fast, ctr, st);
-    case 4: return launch_k1_wf<LANES, VEC, 4>(m, b, n_neg, fast, ctr, st);
-    case 5: return launch_k1_wf<LANES, VEC, 5>(m, b, n_neg, fast, ctr, st);
+    case 1: return launch_k1_wf<LANES, VEC, 1>(m, b, n_neg, fast, ctr, st, resident);
+    case 2: return launch_k1_wf<LANES, VEC, 2>(m, b, n_neg, fast, ctr, st, resident);
+    case 3: return launch_k1_wf<LANES, VEC, 3>(m, b, n_neg, fast, ctr, st, resident);
+    case 4: return launch_k1_wf<LANES, VEC, 4>(m, b, n_neg, fast, ctr, st, resident);
+    case 5: return launch_k1_wf<LANES, VEC, 5>(m, b, n_neg, fast, ctr, st, resident);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -568,9 +569,9 @@ cudaError_t launch_k1_shape(const ModelView& m, const BatchView& b, int n_neg, i
     X(32, 6) X(32, 8) X(32, 10) X(32, 12) X(32, 16)
 
 cudaError_t launch_k1(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf,
-                      bool fast, DevCounters* ctr, cudaStream_t st) {
+                      bool fast, DevCounters* ctr, cudaStream_t st, int* resident) {
 #define FW2V_CASE(L_, V_) \
-    if (lanes == L_ && vec == V_) return launch_k1_shape<L_, V_>(m, b, n_neg, wf, fast, ctr, st);
+    if (lanes == L_ && vec == V_) return launch_k1_shape<L_, V_>(m, b, n_neg, wf, fast, ctr, st, resident);
     FW2V_K1_SHAPES(FW2V_CASE)
 #undef FW2V_CASE
     return cudaErrorInvalidValue;

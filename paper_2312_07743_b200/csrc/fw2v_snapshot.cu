@@ -465,7 +465,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 // ------------------------------------------------------------------ dispatch
 template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
 cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, int n_neg, DevCounters* ctr,
-                            cudaStream_t st) {
+                            cudaStream_t st, int* resident) {
     constexpr int bytes = K1sSmem<LANES, VEC, WF, NC>::kBlockBytes;
     auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MULTI, FAST>;
     static bool configured = false;  // benign race: idempotent attribute set
@@ -474,38 +474,39 @@ cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, 
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    if (resident != nullptr) return resident_sentences(kern, bytes, kK1Threads / LANES, resident);
+    if (blocks == 0) return cudaSuccess;
     kern<<<blocks, kK1Threads, bytes, st>>>(m, b, n_neg, ctr);
     return cudaGetLastError();
 }
 
 template <int LANES, int VEC, int WF, int NC>
 cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
-                          cudaStream_t st) {
+                          cudaStream_t st, int* resident) {
     constexpr int GPW = 32 / LANES;
     const int warps = (b.n_sentences + GPW - 1) / GPW;
     const int blocks = (warps * 32 + kK1Threads - 1) / kK1Threads;
-    if (blocks == 0) return cudaSuccess;
     const bool multi = n_neg + 1 > NC;
     if (multi) {
-        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, true, true>(blocks, m, b, n_neg, ctr, st)
-                    : launch_k1s_inst<LANES, VEC, WF, NC, true, false>(blocks, m, b, n_neg, ctr, st);
+        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, true, true>(blocks, m, b, n_neg, ctr, st, resident)
+                    : launch_k1s_inst<LANES, VEC, WF, NC, true, false>(blocks, m, b, n_neg, ctr, st, resident);
     }
-    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, false, true>(blocks, m, b, n_neg, ctr, st)
-                : launch_k1s_inst<LANES, VEC, WF, NC, false, false>(blocks, m, b, n_neg, ctr, st);
+    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, false, true>(blocks, m, b, n_neg, ctr, st, resident)
+                : launch_k1s_inst<LANES, VEC, WF, NC, false, false>(blocks, m, b, n_neg, ctr, st, resident);
 }
 
 template <int LANES, int VEC>
 cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
-                             DevCounters* ctr, cudaStream_t st) {
+                             DevCounters* ctr, cudaStream_t st, int* resident) {
     switch (wf) {
-    case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, ctr, st);
-    case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, ctr, st);
-    case 3: return launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, ctr, st);
+    case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, ctr, st, resident);
+    case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, ctr, st, resident);
+    case 3: return launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, ctr, st, resident);
     // Wide windows: one 6-sample chunk when N+1 <= 6, else 4-sample chunks (registers).
-    case 4: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 4, 6>(m, b, n_neg, fast, ctr, st)
-                                  : launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, ctr, st);
-    case 5: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 5, 6>(m, b, n_neg, fast, ctr, st)
-                                  : launch_k1s_nc<LANES, VEC, 5, 4>(m, b, n_neg, fast, ctr, st);
+    case 4: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 4, 6>(m, b, n_neg, fast, ctr, st, resident)
+                                  : launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, ctr, st, resident);
+    case 5: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 5, 6>(m, b, n_neg, fast, ctr, st, resident)
+                                  : launch_k1s_nc<LANES, VEC, 5, 4>(m, b, n_neg, fast, ctr, st, resident);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -514,9 +515,9 @@ cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, 
 
 // Requires n_neg <= 2 * LANES (negatives are distributed two per lane).
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
-                       DevCounters* ctr, cudaStream_t st) {
+                       DevCounters* ctr, cudaStream_t st, int* resident) {
 #define FW2V_CASE(L_, V_) \
-    if (lanes == L_ && vec == V_) return launch_k1s_shape<L_, V_>(m, b, n_neg, wf, fast, ctr, st);
+    if (lanes == L_ && vec == V_) return launch_k1s_shape<L_, V_>(m, b, n_neg, wf, fast, ctr, st, resident);
     FW2V_K1S_SHAPES(FW2V_CASE)
 #undef FW2V_CASE
     return cudaErrorInvalidValue;

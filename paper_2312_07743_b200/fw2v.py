@@ -64,7 +64,7 @@ class CConfig(C.Structure):
         ("ignore_delimiters", C.c_int32),
         ("device", C.c_int32), ("deterministic", C.c_int32), ("sampler", C.c_int32),
         ("fast_sigmoid", C.c_int32), ("k1_lanes", C.c_int32), ("streams", C.c_int32),
-        ("l1_refresh_log2", C.c_int32), ("delta_writeback", C.c_int32),
+        ("l1_refresh_log2", C.c_int32), ("delta_writeback", C.c_int32), ("max_inflight", C.c_int32),
     ]
 
 
@@ -124,6 +124,7 @@ class TrainConfig:
     streams: int = 0
     l1_refresh_log2: int = 5
     delta_writeback: bool = True
+    max_inflight: int = 0
 
     @property
     def context_width(self) -> int:
