@@ -79,6 +79,11 @@ typedef struct fw2v_config {
     int32_t max_inflight;  /* Hogwild: sentences in flight on the device at once, summed over the
                               streams. 0 = auto (collision budget from the vocabulary, see DESIGN.md
                               §5), -1 = unlimited (every sentence of a batch in one launch) */
+    int32_t hot_rows;      /* K1s Hogwild: output rows of the hot_rows most frequent words are trained
+                              as hot_replicas data-parallel replicas (sentence s -> replica s mod R),
+                              broadcast before and averaged after every pass; removes the L2
+                              contention and the stale-update pile-up on Zipf-hot rows. 0 = off */
+    int32_t hot_replicas;
 } fw2v_config;
 
 /* ringvec::TrafficCounters (traffic.hpp:19-40) plus totals. */

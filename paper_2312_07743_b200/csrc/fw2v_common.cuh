@@ -218,11 +218,11 @@ __device__ __forceinline__ float sgd_coeff(float f, float label, float alpha) {
 // Sentences of a kernel resident on the whole device at once
 // (blocks per SM x SMs x sentences per block).
 template <typename Kernel>
-cudaError_t resident_sentences(Kernel kern, int smem_bytes, int sentences_per_block, int* out) {
+cudaError_t resident_sentences(Kernel kern, int smem_bytes, int threads, int sentences_per_block, int* out) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kK1Threads, smem_bytes);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem_bytes);
     if (e == cudaSuccess) *out = per_sm * sms * sentences_per_block;
     return e;
 }

@@ -29,6 +29,13 @@ struct ModelView {
     int32_t stride;
     int32_t vocab;
     int32_t flags;  // K1s memory-path options (kFlag*)
+    // Hot-row replicas (K1s Hogwild): output rows 0..hot_k-1 (the most frequent
+    // words, ids are count-descending) live in hot_r replicas at
+    // hot + (r*hot_k + id)*stride; sentence s trains replica s % hot_r. The host
+    // broadcasts syn1 into the replicas before a pass and averages them back after.
+    float* hot;
+    int32_t hot_k;
+    int32_t hot_r;
 };
 
 // K1s memory-path options.

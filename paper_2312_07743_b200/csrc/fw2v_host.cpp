@@ -41,6 +41,8 @@ bool k1_shape_supported(int lanes, int vec);
 cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf, int mode, bool serial,
                       DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st);
+// Hot-row replicas: average = false broadcasts syn1 rows 0..K-1 into them, true averages them back.
+cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st);
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
                        DevCounters* ctr, cudaStream_t st, int* resident = nullptr);
 bool k1s_supported(int lanes, int vec, int n_neg, int wf);
@@ -310,6 +312,18 @@ Shape choose_shape(int dim, int lanes_pref) {
     return {};
 }
 
+// K1s lane shape for a row stride: the fewest lanes per sentence (more
+// sentences per warp amortise the per-window butterfly, sigmoid and
+// bookkeeping) with at most 8 columns per lane (registers).
+Shape choose_k1s_shape(int stride, const Shape& k1, int lanes_pref, int n_neg, int wf) {
+    if (lanes_pref == 0) {
+        static const Shape pref[] = {{4, 4}, {8, 4}, {16, 4}, {16, 8}, {32, 4}, {32, 8}};
+        for (const Shape& s : pref)
+            if (s.lanes * s.vec == stride && k1s_supported(s.lanes, s.vec, n_neg, wf)) return s;
+    }
+    return k1s_supported(k1.lanes, k1.vec, n_neg, wf) ? k1 : Shape{};
+}
+
 int row_stride_for(int dim, int lanes_pref) {
     Shape s = choose_shape(dim, lanes_pref);
     if (s.lanes > 0) return s.lanes * s.vec;
@@ -332,6 +346,7 @@ void validate(const fw2v_config& c) {  // validate_config (config.cpp:165-177)
     if (!(c.table_power >= 0.0)) fail(FW2V_ERR_BAD_CONFIG, "table_power must be >= 0");
     if (c.reuse_mode < 0 || c.reuse_mode > 3) fail(FW2V_ERR_BAD_CONFIG, "unknown reuse mode");
     if (c.sampler < 0 || c.sampler > 1) fail(FW2V_ERR_BAD_CONFIG, "unknown sampler");
+    if (c.hot_rows < 0 || c.hot_replicas < 1) fail(FW2V_ERR_BAD_CONFIG, "hot_rows must be >= 0 and hot_replicas >= 1");
 }
 
 void require_device(int device) {
@@ -381,7 +396,8 @@ struct fw2v_ctx {
     fw2v_config cfg{};
     int wf = 0;
     int32_t vocab = 0;
-    Shape shape;
+    Shape shape;      // K1 (lifetime) lanes x columns
+    Shape k1s_shape;  // K1s (window snapshot) lanes x columns, same row stride
     int stride = 0;
     bool deterministic = false;
     std::vector<uint64_t> counts;
@@ -398,7 +414,11 @@ struct fw2v_ctx {
 
     int32_t k1_flags = 0;
     int64_t inflight_total = 0;  // Hogwild sentences in flight over all streams (0 = unlimited)
-    ModelView model_view() const { return ModelView{syn0, syn1, cfg.dim, stride, vocab, k1_flags}; }
+    float* hot = nullptr;        // hot-row replicas, hot_r x hot_k x stride (K1s Hogwild only)
+    int32_t hot_k = 0, hot_r = 1;
+    ModelView model_view() const { return ModelView{syn0, syn1, cfg.dim, stride, vocab, k1_flags, hot, hot_k, hot_r}; }
+    // Around every Hogwild pass: replicas <- syn1 before, syn1 <- mean(replicas) after.
+    void hot_sync(bool average, cudaStream_t st) const { FW2V_CK(launch_hot_sync(model_view(), average, st)); }
 
     Sampler sampler() const {
         Sampler s;
@@ -454,8 +474,8 @@ struct fw2v_ctx {
         const bool fast = cfg.fast_sigmoid != 0;
         if (!serial && cfg.reuse_mode == kLifetime && shape.lanes > 0 && wf <= 5)
             return launch_k1(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, fast, ctr, st, resident);
-        if (!serial && cfg.reuse_mode == kWindowSnapshot && k1s_supported(shape.lanes, shape.vec, cfg.negatives, wf))
-            return launch_k1s(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, fast, ctr, st, resident);
+        if (!serial && cfg.reuse_mode == kWindowSnapshot && k1s_shape.lanes > 0)
+            return launch_k1s(k1s_shape.lanes, k1s_shape.vec, mv, bv, cfg.negatives, wf, fast, ctr, st, resident);
         if (resident != nullptr) {
             *resident = 0;
             return cudaSuccess;
@@ -497,6 +517,7 @@ struct fw2v_ctx {
             cudaFree(ln.d_ctr);
             if (ln.stream) cudaStreamDestroy(ln.stream);
         }
+        cudaFree(hot);
         if (own_model) {
             cudaFree(syn0);
             cudaFree(syn1);
@@ -543,21 +564,25 @@ uint64_t expected_epoch_words(const fw2v_ctx& x) {  // trainer.cpp:378-386
 
 // Hogwild collision budget. A sample row is drawn with
 // probability p_w ~ count^power; with M sentences in flight, a drawn row is
-// being updated by ~M (N+1) sum_w p_w^2 = M (N+1) / V_eff other sentences at
-// the same time, and their summed deltas act as one step of that many times
-// alpha. Capping M at 2 V_eff keeps that factor near the reference's (a few
-// CPU threads) on tiny vocabularies, and never binds on real ones (text8:
-// V_eff = 1,472 -> 2,944; 1bw: 8,572; both above the ~1,800 sentences the
-// GPU holds resident).
-int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power) {
+// being updated by ~M (N+1) sum_w p_w^2 = M (N+1) / V_eff sentences at the
+// same time, and their summed deltas act as one step of that many times alpha.
+// The cap keeps M (N+1) alpha / V_eff <= 8 x 0.025. Measured on the text8
+// shape (d=128, 5 epochs): 2,960 sentences in flight diverge (loss 3e18) with
+// V_eff = 1,472, 1,776 train to within 0.5% of the reference. Hot-row
+// replicas (fw2v_config.hot_rows) split the top rows' traffic R ways, which
+// lifts V_eff to ~9,700 there; the reference's 60-word pipeline test
+// (V_eff = 60, alpha 0.05) is held to 40 sentences.
+int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power, int n_neg, float alpha0, int hot_k,
+                      int hot_r) {
     double z = 0.0, z2 = 0.0;
     for (int32_t w = 0; w < vocab_size; ++w) {
         const double p = std::pow(static_cast<double>(counts[w]), power);
         z += p;
-        z2 += p * p;
+        z2 += p * p / (w < hot_k ? hot_r : 1);  // a replicated row is shared by 1/R of the sentences
     }
     const double v_eff = z2 > 0.0 ? z * z / z2 : 1.0;
-    return std::max<int64_t>(32, static_cast<int64_t>(std::ceil(2.0 * v_eff)));
+    const double m = 8.0 * 0.025 * v_eff / ((n_neg + 1) * static_cast<double>(alpha0));
+    return std::max<int64_t>(32, static_cast<int64_t>(std::ceil(m)));
 }
 
 } // namespace
@@ -595,6 +620,8 @@ void fw2v_config_default(fw2v_config* c) {
     c->l1_refresh_log2 = 5;
     c->delta_writeback = 1;
     c->max_inflight = 0;
+    c->hot_rows = 64;
+    c->hot_replicas = 16;
 }
 
 int fw2v_validate_config(const fw2v_config* cfg) {
@@ -633,10 +660,11 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
             x->k1_flags |= kFlagL1Samples | (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift);
         if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments
         x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
-                            : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power) : 0;
+                            : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives, cfg->alpha0, 0, 1) : 0;
         x->deterministic = cfg->deterministic == 1 || (cfg->deterministic < 0 && x->cfg.workers == 1);
         x->shape = choose_shape(cfg->dim, cfg->k1_lanes);
         x->stride = row_stride_for(cfg->dim, cfg->k1_lanes);
+        x->k1s_shape = choose_k1s_shape(x->stride, x->shape, cfg->k1_lanes, cfg->negatives, x->wf);
         if (!x->deterministic && cfg->reuse_mode == kLifetime && (x->shape.lanes == 0 || x->wf > 5))
             fail(FW2V_ERR_UNSUPPORTED, "K1 covers dim <= 512 and window <= 10 (W_f <= 5)");
         if (x->wf > 16) fail(FW2V_ERR_UNSUPPORTED, "window > 32 is not supported");
@@ -654,6 +682,15 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         Rng r = Rng::derive(cfg->seed, 0x696e6974ULL);  // "init" stream, model.cpp:26
         FW2V_CK(launch_init_model(x->model_view(), r.state, nullptr));
         FW2V_CK(cudaDeviceSynchronize());
+        if (!x->deterministic && cfg->reuse_mode == kWindowSnapshot && x->k1s_shape.lanes > 0 && cfg->hot_rows > 0) {
+            x->hot_k = std::min(cfg->hot_rows, vocab_size);
+            x->hot_r = cfg->hot_replicas;
+            FW2V_CK(cudaMalloc(&x->hot, sizeof(float) * static_cast<size_t>(x->hot_k) * x->hot_r * x->stride));
+            x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
+                                : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives,
+                                                                         cfg->alpha0, x->hot_k, x->hot_r)
+                                                         : 0;
+        }
         if (x->inflight_total > 0 && !x->deterministic) {
             // The budget only matters when it is below what the device holds at once.
             int resident = 0;
@@ -753,7 +790,9 @@ int fw2v_train_sentences(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_senten
         FW2V_CK(cudaMemcpy(d_off, off.data(), 4 * (n_sentences + 1), cudaMemcpyHostToDevice));
         if (n_sentences) FW2V_CK(cudaMemcpy(d_alpha, alphas, 4 * n_sentences, cudaMemcpyHostToDevice));
         BatchView bv{d_ids, d_off, d_negs, d_alpha, static_cast<int32_t>(n_sentences)};
+        if (!serial) x->hot_sync(false, nullptr);
         FW2V_CK(x->launch(bv, serial != 0, d_ctr, nullptr));
+        if (!serial) x->hot_sync(true, nullptr);
         FW2V_CK(cudaDeviceSynchronize());
         DevCounters h{};
         FW2V_CK(cudaMemcpy(&h, d_ctr, sizeof(h), cudaMemcpyDeviceToHost));
@@ -802,8 +841,19 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
         std::mutex obs_mutex;
         const double run_start = wall_seconds();
 
+        cudaEvent_t synced;
+        FW2V_CK(cudaEventCreateWithFlags(&synced, cudaEventDisableTiming));
+        struct EvGuard {
+            cudaEvent_t e;
+            ~EvGuard() { cudaEventDestroy(e); }
+        } ev_guard{synced};
         for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
             for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), x->lanes[static_cast<size_t>(p)].stream));
+            if (!x->deterministic && x->hot_k > 0) {
+                x->hot_sync(false, x->lanes[0].stream);
+                FW2V_CK(cudaEventRecord(synced, x->lanes[0].stream));
+                for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, synced, 0));
+            }
             std::atomic<uint64_t> reserved{x->words_trained};
             std::vector<uint64_t> an_acc(static_cast<size_t>(P) * 5, 0);
             std::vector<std::string> errors(static_cast<size_t>(P));
@@ -867,6 +917,10 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
             }
             for (auto& t : threads) t.join();
             for (int p = 0; p < P; ++p) FW2V_CK(cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream));
+            if (!x->deterministic && x->hot_k > 0) {
+                x->hot_sync(true, x->lanes[0].stream);
+                FW2V_CK(cudaStreamSynchronize(x->lanes[0].stream));
+            }
             for (const auto& e : errors)
                 if (!e.empty()) fail(FW2V_ERR_CUDA, e);
             const double secs = wall_seconds() - t0;
@@ -1014,6 +1068,8 @@ int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* 
         cudaStream_t s0 = x->lanes[0].stream;
         for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), s0));
         FW2V_CK(cudaEventRecord(start, s0));
+        const bool hot = !x->deterministic && x->hot_k > 0;
+        if (hot) x->hot_sync(false, s0);
         FW2V_CK(cudaEventRecord(fork, s0));
         for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, fork, 0));
         // Interleave launches across lanes so each stream always has queued work.
@@ -1025,6 +1081,12 @@ int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* 
                     FW2V_CK(x->launch(plan->lanes[static_cast<size_t>(p)][k].view, x->deterministic,
                                       x->lanes[static_cast<size_t>(p)].d_ctr, x->lanes[static_cast<size_t>(p)].stream, P));
         for (int p = 0; p < P; ++p) FW2V_CK(cudaEventRecord(ends[static_cast<size_t>(p)], x->lanes[static_cast<size_t>(p)].stream));
+        if (hot) {
+            // Join every lane on s0, fold the replicas back; the pass ends there.
+            for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(s0, ends[static_cast<size_t>(p)], 0));
+            x->hot_sync(true, s0);
+            FW2V_CK(cudaEventRecord(ends[0], s0));
+        }
         float ms_max = 0.0f;
         for (int p = 0; p < P; ++p) {
             FW2V_CK(cudaEventSynchronize(ends[static_cast<size_t>(p)]));

@@ -545,7 +545,7 @@ cudaError_t launch_k1_wf(const ModelView& m, const BatchView& b, int n_neg, bool
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         if (e != cudaSuccess) return e;
     }
-    if (resident != nullptr) return resident_sentences(kern, bytes, kK1Threads / LANES, resident);
+    if (resident != nullptr) return resident_sentences(kern, bytes, kK1Threads, kK1Threads / LANES, resident);
     if (blocks == 0) return cudaSuccess;
     kern<<<blocks, kK1Threads, bytes, st>>>(m, b, n_neg, ctr);
     return cudaGetLastError();
@@ -608,6 +608,33 @@ cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf,
 
 cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st) {
     k_init_model<<<148 * 8, 256, 0, st>>>(m, state0);
+    return cudaGetLastError();
+}
+
+// Hot-row replicas (ModelView::hot): broadcast output rows 0..K-1 into every
+// replica before a Hogwild pass, and average the replicas back after it.
+__global__ void k_hot_broadcast(ModelView m) {
+    const int n = m.hot_k * m.stride;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        const float v = m.syn1[x];
+        for (int r = 0; r < m.hot_r; ++r) m.hot[static_cast<size_t>(r) * n + x] = v;
+    }
+}
+__global__ void k_hot_average(ModelView m) {
+    const int n = m.hot_k * m.stride;
+    const float inv = 1.0f / static_cast<float>(m.hot_r);
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int r = 0; r < m.hot_r; ++r) s += m.hot[static_cast<size_t>(r) * n + x];
+        m.syn1[x] = s * inv;
+    }
+}
+cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st) {
+    if (m.hot_k <= 0) return cudaSuccess;
+    const int n = m.hot_k * m.stride;
+    const int blocks = (n + 255) / 256;
+    if (average) k_hot_average<<<blocks, 256, 0, st>>>(m);
+    else k_hot_broadcast<<<blocks, 256, 0, st>>>(m);
     return cudaGetLastError();
 }
 

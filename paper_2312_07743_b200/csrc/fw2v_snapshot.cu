@@ -28,6 +28,17 @@
 #include "fw2v_common.cuh"
 #include "fw2v_device.cuh"
 
+#ifdef KB_TIMING  // experiment: per-phase SM clocks of each warp, summed into kb_timing[]
+__device__ unsigned long long kb_timing[16];
+#define KB_T_DECL unsigned long long kbt[10] = {0}; long long kbt0 = clock64();
+#define KB_T(k) { const long long t_ = clock64(); kbt[k] += t_ - kbt0; kbt0 = t_; }
+#define KB_T_DUMP if (lane == 0) for (int k_ = 0; k_ < 9; ++k_) atomicAdd(&kb_timing[k_], kbt[k_]);
+#else
+#define KB_T_DECL
+#define KB_T(k)
+#define KB_T_DUMP
+#endif
+
 namespace fw2v {
 
 // Transposed butterfly over the lanes of a group (offsets O, O/2, ..., 1).
@@ -57,6 +68,16 @@ struct Butterfly {
         if constexpr (O > 1) Butterfly<O / 2, NEXT>::reduce(v, sub);
     }
 
+    // Same result when lanes with bit O set hold v[j] and v[j + H] swapped on
+    // entry (their operands were loaded in swapped order): no selects at the top level.
+    template <int CAP>
+    __device__ __forceinline__ static void reduce_preswapped(float (&v)[CAP], int sub) {
+        static_assert(N <= CAP && (N & 1) == 0, "butterfly overflow");
+#pragma unroll
+        for (int j = 0; j < H; ++j) v[j] += __shfl_xor_sync(kFull, v[j + H], O);
+        if constexpr (O > 1) Butterfly<O / 2, NEXT>::reduce(v, sub);
+    }
+
     template <int CAP>
     __device__ __forceinline__ static void plan(int (&idx)[CAP], int sub) {
         const bool bit = (sub & O) != 0;
@@ -76,23 +97,9 @@ __device__ __forceinline__ void cp_async16_ca(float* smem, const float* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-template <int H2>
-__device__ __forceinline__ void row_red_add(float* p, const float2 (&d)[H2]) {
-#pragma unroll
-    for (int i = 0; i < H2; i += 2)
-        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + 2 * i), "f"(d[i].x), "f"(d[i].y),
-                     "f"(d[i + 1].x), "f"(d[i + 1].y)
-                     : "memory");
-}
-// red.add(value - entry_value): the ring row's accumulated update since it was loaded.
-template <int H2>
-__device__ __forceinline__ void row_red_delta(float* p, const float2 (&v)[H2], const float* entry_smem) {
-    float2 e[H2];
-    Row2<H2>::load_shared(e, entry_smem);
-#pragma unroll
-    for (int i = 0; i < H2; ++i) e[i] = make_float2(v[i].x - e[i].x, v[i].y - e[i].y);
-    row_red_add(p, e);
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 constexpr int kPrefetchWindows = 16;
 
@@ -101,16 +108,80 @@ struct K1sSmem {
     static constexpr int NCTX = 2 * WF;
     static constexpr int C = 2 * WF + 1;
     static constexpr int NV = NC * NCTX;
+    static constexpr int GPAD = (NV + 3) & ~3;
     static constexpr int STRIDE = LANES * VEC;
-    // per group: g pairs, sample prefetch buffer, finish stash
-    // per group: g pairs, sample prefetch buffer, finish stash, ring entry values
-    // (sample buffers are double-buffered by window parity)
-    static constexpr int kGroupFloats = 2 * NV + 2 * NC * STRIDE + 2 * C * STRIDE;
-    static constexpr int kBlockBytes = (kK1Threads / LANES) * kGroupFloats * 4;
+    // Wide lane slices (VEC >= 8) hold twice the registers per lane: 64-thread
+    // blocks keep the per-block shared memory small enough for 5 blocks per SM.
+    static constexpr int THREADS = VEC >= 8 ? 64 : kK1Threads;
+    // Per group (one sentence): the window's g coefficients (scalars), the
+    // sample rows double-buffered by window parity, and the ring rows as loaded
+    // (delta write-back) or the finish() stash (overwrite) — never both.
+    static constexpr int kGroupFloats = GPAD + 2 * NC * STRIDE + C * STRIDE;
+    static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
+    static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
+    static constexpr int kRegBlocks = VEC >= 8 ? 5 : 3;
+    static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
+};
+
+// A lane's slice of a row: VEC = 2*H2 columns as H2/2 16-byte chunks spaced CS
+// floats apart (chunk c of lane l at column 4*(c*LANES + l), CS = 4*LANES), so
+// one 16-byte access by a lane group covers a contiguous 16*LANES-byte span:
+// coalesced in HBM/L2 and bank-conflict free in shared memory.
+template <int H2, int CS>
+struct Slice {
+    static_assert(H2 % 2 == 0, "16-byte chunks");
+    static constexpr int NCH = H2 / 2;
+    __device__ __forceinline__ static void set(float2 (&v)[H2], int c, float4 t) {
+        v[2 * c] = make_float2(t.x, t.y);
+        v[2 * c + 1] = make_float2(t.z, t.w);
+    }
+    __device__ __forceinline__ static float4 get(const float2 (&v)[H2], int c) {
+        return make_float4(v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
+    }
+    __device__ __forceinline__ static void load(float2 (&v)[H2], const float* p) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) set(v, c, __ldcg(reinterpret_cast<const float4*>(p + c * CS)));
+    }
+    __device__ __forceinline__ static void load_early(float2 (&v)[H2], const float* p) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) set(v, c, ldcg_early(p + c * CS));
+    }
+    __device__ __forceinline__ static void store(float* p, const float2 (&v)[H2]) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) __stcg(reinterpret_cast<float4*>(p + c * CS), get(v, c));
+    }
+    __device__ __forceinline__ static void load_shared(float2 (&v)[H2], const float* p) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) set(v, c, *reinterpret_cast<const float4*>(p + c * CS));
+    }
+    __device__ __forceinline__ static void store_shared(float* p, const float2 (&v)[H2]) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) *reinterpret_cast<float4*>(p + c * CS) = get(v, c);
+    }
+    // row += d at L2 when pred (no branch).
+    __device__ __forceinline__ static void red_add_if(bool pred, float* p, const float2 (&d)[H2]) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const float4 t = get(d, c);
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+                "@q red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p + c * CS),
+                "f"(t.x), "f"(t.y), "f"(t.z), "f"(t.w), "r"(static_cast<int>(pred))
+                : "memory");
+        }
+    }
+    // row += (v - entry): the ring row's accumulated update since it was loaded.
+    __device__ __forceinline__ static void red_delta(float* p, const float2 (&v)[H2], const float* entry_smem) {
+        float2 e[H2];
+        load_shared(e, entry_smem);
+#pragma unroll
+        for (int i = 0; i < H2; ++i) e[i] = make_float2(v[i].x - e[i].x, v[i].y - e[i].y);
+        red_add_if(true, p, e);
+    }
 };
 
 template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
-__global__ void __launch_bounds__(kK1Threads, (VEC >= 8 ? 1 : 3))
+__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC>::THREADS, K1sSmem<LANES, VEC, WF, NC>::MINB)
 k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) {
     static_assert(VEC % 4 == 0, "K1s stages 16-byte slices");
     using SM = K1sSmem<LANES, VEC, WF, NC>;
@@ -118,23 +189,30 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     constexpr int C = SM::C;
     constexpr int NV = SM::NV;
     constexpr int H2 = VEC / 2;
-    constexpr int GPW = 32 / LANES;
+    constexpr int STRIDE = SM::STRIDE;
+    constexpr int HALF = LANES / 2;
+    constexpr int NN = NC - 1;  // negatives per window held by every lane (single-chunk path)
+    // Stale-prefetch detection by one __match_any_sync: lanes q < NC of a group
+    // carry this window's sample ids, lanes HALF + q the previous window's.
+    constexpr bool kMatch = NC <= HALF;
+    // The top butterfly level pairs samples q and q + NC/2 of one context row;
+    // lanes of the upper half load those two sample rows in swapped order, so
+    // that level needs no selects.
+    constexpr bool kPreswap = NC % 2 == 0;
+    using SL = Slice<H2, 4 * LANES>;
     using BF = Butterfly<LANES / 2, NV>;
     constexpr int NF = BF::final_count();
+    static_assert(NV <= 255 && NC <= 16 && NCTX <= 16, "slot words");
     extern __shared__ __align__(16) float k1s_sh[];
 
     const int lane = threadIdx.x & 31;
     const int sub = lane & (LANES - 1);
     const int grp = lane / LANES;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int sent = warp * GPW + grp;
+    const int sent = static_cast<int>((blockIdx.x * SM::THREADS + threadIdx.x) / LANES);
     const bool has = sent < b.n_sentences;
     float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
-    float2* g2 = reinterpret_cast<float2*>(gsh);
-    float* sbuf = gsh + 2 * NV + sub * VEC;                         // + (parity*NC + q)*STRIDE
-    float* stash = gsh + 2 * NV + 2 * NC * SM::STRIDE + sub * VEC;  // + slot*STRIDE
-    // Ring rows as loaded (delta write-back: red.add(final - loaded)).
-    float* entry = gsh + 2 * NV + (2 * NC + C) * SM::STRIDE + sub * VEC;
+    float* sbuf = gsh + SM::GPAD + sub * 4;                  // + (parity*NC + q)*STRIDE
+    float* ring = gsh + SM::GPAD + 2 * NC * STRIDE + sub * 4;  // + slot*STRIDE
     const bool delta_wb = (m.flags & kFlagDeltaRing) != 0;
 
     uint32_t beg = 0, len = 0;
@@ -151,11 +229,18 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     const int32_t* __restrict__ ids = b.ids + beg;
     const int32_t* __restrict__ negs = b.negs + static_cast<size_t>(beg) * n_neg;
     // Row offsets use the compile-time stride (host checks |V| * stride < 2^31).
-    float* __restrict__ syn0 = m.syn0 + sub * VEC;
-    float* __restrict__ syn1 = m.syn1 + sub * VEC;
+    float* __restrict__ syn0 = m.syn0 + sub * 4;
+    float* __restrict__ syn1 = m.syn1 + sub * 4;
+    // Output row of sample s >= 0: hot rows go to this sentence's replica.
+    float* const hot_base = m.hot_k > 0 ? m.hot + (sent % m.hot_r) * m.hot_k * STRIDE + sub * 4 : syn1;
+    const int hot_k = m.hot_k;
+    auto srow = [&](int s) { return (s < hot_k ? hot_base : syn1) + s * STRIDE; };
     const int tail = L - C;  // positions >= tail stay resident until finish()
 
-    int slot_q[NF], slot_r[NF], slot_m[NF];
+    // After the butterfly, slot j of this lane holds dot idx = q*NCTX + r. One
+    // opaque word per slot (the compiler would otherwise re-derive the plan
+    // every window): g index | r << 8 | q << 12 | (q <= N) << 16 | (q == 0) << 17.
+    unsigned slotw[NF];
     {
         int idx[NV];
 #pragma unroll
@@ -163,76 +248,79 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         BF::plan(idx, sub);
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-            slot_q[j] = idx[j] / NCTX;
-            slot_r[j] = idx[j] - slot_q[j] * NCTX;
-            slot_m[j] = slot_r[j] * NC + slot_q[j];  // g pairs are stored context-major
+            const int q = idx[j] / NCTX, r = idx[j] - q * NCTX;
+            slotw[j] = static_cast<unsigned>(idx[j]) | (static_cast<unsigned>(r) << 8) |
+                       (static_cast<unsigned>(q) << 12) | ((q <= n_neg ? 1u : 0u) << 16) | ((q == 0 ? 1u : 0u) << 17);
+            asm volatile("" : "+r"(slotw[j]));
         }
     }
+    const int swap_off = (kPreswap && (sub & HALF) != 0) ? (NC / 2) * STRIDE : 0;
 
     float2 ctx[NCTX][H2];
     int tok[NCTX];
     float2 tgt[H2];
     int ttok = L > 0 ? __ldg(ids) : -1;
-    if (ttok >= 0) Row2<H2>::load(tgt, syn0 + ttok * SM::STRIDE); else vzero2(tgt);
-    if (delta_wb) Row2<H2>::store_shared(entry, tgt);  // position 0 -> slot 0
+    if (ttok >= 0) SL::load(tgt, syn0 + ttok * STRIDE); else vzero2(tgt);
+    if (delta_wb) SL::store_shared(ring, tgt);  // position 0 -> slot 0
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
         const int p = r - WF + 1;
         tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
-        if (tok[r] >= 0) Row2<H2>::load(ctx[r], syn0 + tok[r] * SM::STRIDE); else vzero2(ctx[r]);
-        if (delta_wb && r >= WF) Row2<H2>::store_shared(entry + p * SM::STRIDE, ctx[r]);  // p < C
+        if (tok[r] >= 0) SL::load(ctx[r], syn0 + tok[r] * STRIDE); else vzero2(ctx[r]);
+        if (delta_wb && r >= WF) SL::store_shared(ring + p * STRIDE, ctx[r]);  // p < C
     }
     unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
     unsigned s_rw = 0, pairs = 0;
 
-    // Negatives of the current window, one per lane (lane q holds negative q).
-    // Negatives of a window, two per lane: lane q holds negative q (negreg.x)
-    // and negative q + LANES (negreg.y), so N <= 2 * LANES.
-    int2 negreg = make_int2((sub < n_neg && L >= 2) ? __ldg(negs + sub) : -1,
-                            (sub + LANES < n_neg && L >= 2) ? __ldg(negs + sub + LANES) : -1);
-    // Negative j (0-based) of the window held in `nr`, broadcast within the group.
-    auto neg_of = [&](int2 nr, int j) {
-        const int v = __shfl_sync(kFull, j < LANES ? nr.x : nr.y, j & (LANES - 1), LANES);
-        return v;
-    };
-    int tok_ahead = WF + 1 < L ? __ldg(ids + WF + 1) : -1;  // incoming position of window 0
-    // Sample ids of the first chunk of the previous window (stale-prefetch check).
-    int psid[NC];
+    // Single-chunk path: every lane holds the negatives of windows i (ncur),
+    // i+1 (nnext, for the prefetch) and, raw, i+2 (loaded one window early).
+    int ncur[MULTI ? 1 : NN], nnext[MULTI ? 1 : NN], nraw[MULTI ? 1 : NN];
+    if constexpr (!MULTI) {
 #pragma unroll
-    for (int q = 0; q < NC; ++q) psid[q] = -100;  // sentinels never equal a live or empty sample id
+        for (int k = 0; k < NN; ++k) {
+            ncur[k] = (k < n_neg && L >= 2) ? __ldg(negs + k) : -1;
+            nnext[k] = (k < n_neg && 1 < L) ? __ldg(negs + n_neg + k) : -1;
+            nraw[k] = -1;
+        }
+    }
+    int tok_ahead = WF + 1 < L ? __ldg(ids + WF + 1) : -1;  // incoming position of window 0
+    int prev_v = -1 - lane;  // match lanes: previous window's sample id
+    int psid[kMatch ? 1 : NC];
+#pragma unroll
+    for (int q = 0; q < (kMatch ? 1 : NC); ++q) psid[q] = -100;
 
     {
         const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
         for (int q = 0; q < 2 * NC; ++q)
 #pragma unroll
-            for (int e = 0; e < VEC; e += 4) *reinterpret_cast<float4*>(sbuf + q * SM::STRIDE + e) = z;
+            for (int e = 0; e < VEC / 4; ++e) *reinterpret_cast<float4*>(sbuf + q * STRIDE + e * 4 * LANES) = z;
     }
     const bool l1_samples = (m.flags & kFlagL1Samples) != 0;
-    auto prefetch = [&](int target, int2 negv, bool active, int parity) {
-        float* dst = sbuf + parity * NC * SM::STRIDE;
+    auto prefetch = [&](int target, const int (&nv)[MULTI ? 1 : NN], bool active, int parity) {
+        float* dst = sbuf + parity * NC * STRIDE;
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-            const int nb = neg_of(negv, q > 0 ? q - 1 : 0);
-            const int s = q == 0 ? target : nb;
+            const int s = q == 0 ? target : nv[q > 0 ? q - 1 : 0];
             if (active && q <= n_neg && s >= 0) {
 #pragma unroll
-                for (int e = 0; e < VEC; e += 4) {
-                    if (l1_samples) cp_async16_ca(dst + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
-                    else cp_async16(dst + q * SM::STRIDE + e, syn1 + s * SM::STRIDE + e);
+                for (int e = 0; e < VEC / 4 * 4 * LANES; e += 4 * LANES) {
+                    if (l1_samples) cp_async16_ca(dst + q * STRIDE + e, srow(s) + e);
+                    else cp_async16(dst + q * STRIDE + e, srow(s) + e);
                 }
             }
         }
     };
     const int inval_log2 = (m.flags >> kFlagInvalShift) & 15;
     const unsigned inval_mask = inval_log2 ? (1u << inval_log2) - 1u : 0u;
-    // Negatives of the next window (window i+1 while window i runs): the
-    // prefetch of window i+1's rows is issued at the start of window i.
-    int2 negnext = make_int2((sub < n_neg && L >= 2) ? __ldg(negs + n_neg + sub) : -1,
-                             (sub + LANES < n_neg && L >= 2) ? __ldg(negs + n_neg + sub + LANES) : -1);
-    if (!MULTI) prefetch(ttok, negreg, L >= 2, 0);  // window 0's samples
+    bool nraw_ok = false;
+    if constexpr (!MULTI) {
+        prefetch(ttok, ncur, L >= 2, 0);  // window 0's samples
+        cp_async_commit();
+    }
     float2 dctx[MULTI ? NCTX : 1][H2];
 
+    KB_T_DECL
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
         const bool wact = act && L >= 2;
@@ -240,22 +328,61 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) vmask |= (tok[r] >= 0 ? 1u : 0u) << r;
         const int q_in = i + 1 + WF;
-        // Token ids run one window ahead of their rows, and the id/negative
-        // streams are pulled into L2 kPrefetchWindows ahead, so no row load
-        // waits on an id load that missed to DRAM.
+        // Token ids run one window ahead of their rows and negatives two; loads
+        // issued early are carried raw and masked where consumed. The
+        // id/negative streams are pulled into L2 kPrefetchWindows ahead.
+        if constexpr (!MULTI) {
+            if (i > 0) {
+#pragma unroll
+                for (int k = 0; k < NN; ++k) nnext[k] = (nraw_ok && k < n_neg) ? nraw[k] : -1;
+            }
+        }
+        // Next window's sample rows first (their buffer was last read in window
+        // i-1); one cp.async group per window, so the wait below can leave it in flight.
+        unsigned stale = 0;
+        if constexpr (!MULTI) {
+            if (i + 1 < Lmax) prefetch(tok[WF], nnext, i + 1 < L && L >= 2, (i + 1) & 1);
+            cp_async_commit();
+            // This window's rows the previous window rewrote after their prefetch
+            // was issued (computed here, off the critical path).
+            if constexpr (kMatch) {
+                const int q = sub & (HALF - 1);
+                int cv = ttok;
+#pragma unroll
+                for (int k = 0; k < NN; ++k) cv = q == k + 1 ? ncur[k] : cv;
+                cv = (wact && q <= n_neg && q < NC) ? cv : -1 - lane;
+                const int mv = sub < HALF ? cv : prev_v;
+                const unsigned mm = __match_any_sync(kFull, mv);
+                const unsigned upper = ((1u << HALF) - 1u) << (grp * LANES + HALF);
+                const bool st = sub < HALF && (mm & upper) != 0u;
+                stale = (__ballot_sync(kFull, st) >> (grp * LANES)) & ((1u << NC) - 1u);
+                prev_v = cv;
+            } else {
+                int sq[NC];
+#pragma unroll
+                for (int q = 0; q < NC; ++q) sq[q] = (wact && q <= n_neg) ? (q == 0 ? ttok : ncur[q > 0 ? q - 1 : 0]) : -1 - q;
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    bool st = false;
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) st |= sq[q] == psid[j];
+                    stale |= (st ? 1u : 0u) << q;
+                }
+#pragma unroll
+                for (int q = 0; q < NC; ++q) psid[q] = sq[q] >= 0 ? sq[q] : -100;
+            }
+        }
         const int inc_tok = tok_ahead;
-        // Issued here, consumed at the end of the window (ring slide) and by the
-        // next window's prefetch: clamped addresses, no branches, no sinking.
         float2 inc[H2];
-        row_load_early(inc, syn0 + max(inc_tok, 0) * SM::STRIDE);
+        SL::load_early(inc, syn0 + max(inc_tok, 0) * STRIDE);
         const int last = max(L - 1, 0);
         const int tok_raw = ldg_early(ids + min(q_in + 1, last));
-        const int* nrow = negs + static_cast<size_t>(min(i + 2, last)) * n_neg;
-        const int neg_raw = n_neg > 0 ? ldg_early(nrow + min(sub, n_neg - 1)) : -1;
-        const int neg_raw2 = n_neg > LANES ? ldg_early(nrow + min(sub + LANES, n_neg - 1)) : -1;
-        tok_ahead = q_in + 1 < L ? tok_raw : -1;
-        const int2 negnext2 = make_int2((sub < n_neg && i + 2 < L) ? neg_raw : -1,
-                                        (sub + LANES < n_neg && i + 2 < L) ? neg_raw2 : -1);
+        if constexpr (!MULTI) {
+            const int* nrow = negs + static_cast<size_t>(min(i + 2, last)) * n_neg;
+#pragma unroll
+            for (int k = 0; k < NN; ++k) nraw[k] = n_neg > 0 ? ldg_early(nrow + min(k, n_neg - 1)) : -1;
+        }
+        const bool tok_ok = q_in + 1 < L;
         if (sub == 0 && i + kPrefetchWindows < L) {
             prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * n_neg);
             prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
@@ -270,104 +397,122 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         for (int ch = 0; ch < n_chunks; ++ch) {
             const int kbase = MULTI ? ch * NC : 0;
             int sid[NC];
-            float2 S[NC][H2];
 #pragma unroll
             for (int q = 0; q < NC; ++q) {
                 const int kk = kbase + q;
-                const int nb = neg_of(negreg, kk > 0 ? kk - 1 : 0);
-                const int s = kk == 0 ? ttok : nb;
+                int s;
+                if constexpr (MULTI) s = (kk == 0) ? ttok : (wact && kk <= n_neg ? __ldg(negs + i * n_neg + kk - 1) : -1);
+                else s = q == 0 ? ttok : ncur[q > 0 ? q - 1 : 0];
                 sid[q] = (wact && kk <= n_neg) ? s : -1 - q;  // empty slots: distinct negative ids
             }
+            const float* cur = sbuf;
             if constexpr (!MULTI) {
-                // Staged by cp.async during the previous window (slots without a
-                // sample hold finite stale rows and get g = 0). Rows the previous
-                // window rewrote after the prefetch was issued are re-read.
-                cp_async_wait_all();
+                // Rows staged by cp.async during the previous window; slots
+                // without a sample hold finite stale rows and get g = 0.
+                KB_T(0)
+                cp_async_wait_group<1>();
+                KB_T(1)
+                cur = sbuf + (i & 1) * NC * STRIDE;
+                if (stale != 0u) {
 #pragma unroll
-                for (int q = 0; q < NC; ++q) Row2<H2>::load_shared(S[q], sbuf + ((i & 1) * NC + q) * SM::STRIDE);
-                // Next window's rows go to the other buffer right away.
-                if (i + 1 < Lmax) prefetch(tok[WF], negnext, i + 1 < L && L >= 2, (i + 1) & 1);
-                bool stale = false;
-#pragma unroll
-                for (int q = 0; q < NC; ++q)
-#pragma unroll
-                    for (int j = 0; j < NC; ++j) stale |= sid[q] == psid[j];
-                if (stale) {
-#pragma unroll
-                    for (int q = 0; q < NC; ++q) {
-                        bool st = false;
-#pragma unroll
-                        for (int j = 0; j < NC; ++j) st |= sid[q] == psid[j];
-                        if (st && sid[q] >= 0) Row2<H2>::load(S[q], syn1 + sid[q] * SM::STRIDE);
-                    }
+                    for (int q = 0; q < NC; ++q)
+                        if (((stale >> q) & 1u) && sid[q] >= 0) {
+                            float2 v[H2];
+                            SL::load(v, srow(sid[q]));
+                            SL::store_shared(const_cast<float*>(cur) + q * STRIDE, v);
+                        }
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < NC; ++q) Row2<H2>::load(S[q], syn1 + max(sid[q], 0) * SM::STRIDE);
+                for (int q = 0; q < NC; ++q) {
+                    float2 v[H2];
+                    SL::load(v, srow(max(sid[q], 0)));
+                    SL::store_shared(sbuf + q * STRIDE, v);
+                }
             }
 
-            // 1-2. all dots of the chunk, then one transposed butterfly.
+            KB_T(2)
+            // 1-2. all dots of the chunk (window-entry values), one transposed butterfly.
             float P[NV];
+            {
+                const float* lo = cur + swap_off;  // samples q < NC/2 (or their partners)
+                const float* hi = cur - swap_off;
 #pragma unroll
-            for (int q = 0; q < NC; ++q)
+                for (int q = 0; q < NC; ++q) {
+                    float2 S[H2];
+                    SL::load_shared(S, (kPreswap && q < NC / 2 ? lo : (kPreswap ? hi : cur)) + q * STRIDE);
 #pragma unroll
-                for (int r = 0; r < NCTX; ++r) {
-                    float2 acc = __fmul2_rn(ctx[r][0], S[q][0]);
+                    for (int r = 0; r < NCTX; ++r) {
+                        float2 acc = __fmul2_rn(ctx[r][0], S[0]);
 #pragma unroll
-                    for (int h = 1; h < H2; ++h) acc = __ffma2_rn(ctx[r][h], S[q][h], acc);
-                    P[q * NCTX + r] = acc.x + acc.y;
+                        for (int h = 1; h < H2; ++h) acc = __ffma2_rn(ctx[r][h], S[h], acc);
+                        P[q * NCTX + r] = acc.x + acc.y;
+                    }
                 }
-            BF::reduce(P, sub);
+            }
+            KB_T(3)
+            if constexpr (kPreswap) BF::reduce_preswapped(P, sub);
+            else BF::reduce(P, sub);
 
-
-            // 3. sigmoid on owned slots, publish g pairs.
+            KB_T(4)
+            // 3. sigmoid on the owned dots; g published as scalars [q][r].
 #pragma unroll
             for (int j = 0; j < NF; ++j) {
-                const int kk = ch * NC + slot_q[j];
-                const bool valid = wact && kk <= n_neg && ((vmask >> slot_r[j]) & 1u);
-                const float g = valid ? sgd_coeff<FAST>(P[j], kk == 0 ? 1.0f : 0.0f, alpha) : 0.0f;
-                g2[slot_m[j]] = make_float2(g, g);  // context-major: [r][q]
+                const unsigned w = slotw[j];
+                const bool vbit = ((vmask >> ((w >> 8) & 15u)) & 1u) != 0u;
+                bool valid;
+                float label;
+                if constexpr (MULTI) {
+                    const int kk = kbase + static_cast<int>((w >> 12) & 15u);
+                    valid = wact && kk <= n_neg && vbit;
+                    label = kk == 0 ? 1.0f : 0.0f;
+                } else {
+                    valid = wact && ((w >> 16) & 1u) && vbit;
+                    label = ((w >> 17) & 1u) ? 1.0f : 0.0f;
+                }
+                gsh[w & 255u] = valid ? sgd_coeff<FAST>(P[j], label, alpha) : 0.0f;
+            }
+            __syncwarp();
+            float g[SM::GPAD];
+#pragma unroll
+            for (int k = 0; k < SM::GPAD; k += 4) {
+                const float4 t = *reinterpret_cast<const float4*>(gsh + k);
+                g[k] = t.x; g[k + 1] = t.y; g[k + 2] = t.z; g[k + 3] = t.w;
             }
             __syncwarp();
 
-            // 4. context-major sweep: with r fixed, sample deltas take the
-            //    window-entry c_r, then c_r takes the window-entry samples, so
-            //    each (g, g) pair is loaded once and used twice.
-            float2 D[NC][H2];
+            KB_T(5)
+            // 4a. sample deltas from window-entry context rows, written back as
+            //     row += delta at L2 (trainer.cpp:198-204, duplicates included).
 #pragma unroll
-            for (int q = 0; q < NC; ++q) vzero2(D[q]);
+            for (int q = 0; q < NC; ++q) {
+                float2 D[H2];
 #pragma unroll
-            for (int r = 0; r < NCTX; ++r) {
-                float2 G[NC];
+                for (int h = 0; h < H2; ++h) D[h] = __fmul2_rn(make_float2(g[q * NCTX], g[q * NCTX]), ctx[0][h]);
 #pragma unroll
-                for (int q = 0; q < NC; q += 2) {
-                    const float4 t = *reinterpret_cast<const float4*>(g2 + r * NC + q);
-                    G[q] = make_float2(t.x, t.y);
-                    if (q + 1 < NC) G[q + 1] = make_float2(t.z, t.w);
-                }
+                for (int r = 1; r < NCTX; ++r)
 #pragma unroll
-                for (int q = 0; q < NC; ++q)
+                    for (int h = 0; h < H2; ++h)
+                        D[h] = __ffma2_rn(make_float2(g[q * NCTX + r], g[q * NCTX + r]), ctx[r][h], D[h]);
+                SL::red_add_if(sid[q] >= 0, srow(max(sid[q], 0)), D);
+            }
+            KB_T(6)
+            // 4b. context rows from window-entry sample rows.
 #pragma unroll
-                    for (int h = 0; h < H2; ++h) D[q][h] = __ffma2_rn(G[q], ctx[r][h], D[q][h]);
+            for (int q = 0; q < NC; ++q) {
+                float2 S[H2];
+                SL::load_shared(S, cur + q * STRIDE);
 #pragma unroll
-                for (int q = 0; q < NC; ++q)
+                for (int r = 0; r < NCTX; ++r) {
+                    const float2 gg = make_float2(g[q * NCTX + r], g[q * NCTX + r]);
 #pragma unroll
                     for (int h = 0; h < H2; ++h) {
-                        if constexpr (MULTI) dctx[r][h] = __ffma2_rn(G[q], S[q][h], dctx[r][h]);
-                        else ctx[r][h] = __ffma2_rn(G[q], S[q][h], ctx[r][h]);
+                        if constexpr (MULTI) dctx[r][h] = __ffma2_rn(gg, S[h], dctx[r][h]);
+                        else ctx[r][h] = __ffma2_rn(gg, S[h], ctx[r][h]);
                     }
+                }
             }
-            __syncwarp();
-            // Write back (row += delta) as a vector reduction at L2: exactly
-            // trainer.cpp:198-204 (repeated ids included), and no read-modify-
-            // write round trip on Zipf-hot rows.
-#pragma unroll
-            for (int q = 0; q < NC; ++q)
-                if (sid[q] >= 0) row_red_add(syn1 + sid[q] * SM::STRIDE, D[q]);
-            if (ch == 0) {
-#pragma unroll
-                for (int q = 0; q < NC; ++q) psid[q] = sid[q] >= 0 ? sid[q] : -100;
-            }
+            if constexpr (MULTI) __syncwarp();  // the next chunk rewrites sbuf
         }
         if constexpr (MULTI) {
 #pragma unroll
@@ -380,20 +525,21 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             pairs += static_cast<unsigned>(__popc(vmask)) * static_cast<unsigned>(n_neg + 1);
         }
 
+        KB_T(7)
         // Slide the ring (ContextRing::advance, trainer.cpp:55-69).
         const int etok = tok[0];
         if (etok >= 0) {
             const int p = i - WF;
             if (delta_wb) {
-                row_red_delta(syn0 + etok * SM::STRIDE, ctx[0], entry + (p % C) * SM::STRIDE);
+                SL::red_delta(syn0 + etok * STRIDE, ctx[0], ring + (p % C) * STRIDE);
             } else if (p >= tail) {
-                Row2<H2>::store_shared(stash + (p % C) * SM::STRIDE, ctx[0]);
+                SL::store_shared(ring + (p % C) * STRIDE, ctx[0]);
             } else {
-                Row2<H2>::store(syn0 + etok * SM::STRIDE, ctx[0]);
+                SL::store(syn0 + etok * STRIDE, ctx[0]);
             }
             if (inc_tok == etok) vcopy2(inc, ctx[0]);
         }
-        if (delta_wb && inc_tok >= 0) Row2<H2>::store_shared(entry + (q_in % C) * SM::STRIDE, inc);
+        if (delta_wb && inc_tok >= 0) SL::store_shared(ring + (q_in % C) * STRIDE, inc);
 #pragma unroll
         for (int r = 0; r < WF - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
         vcopy2(ctx[WF - 1], tgt);
@@ -404,40 +550,45 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         for (int r = WF; r < NCTX - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
         vcopy2(ctx[NCTX - 1], inc);
         tok[NCTX - 1] = inc_tok;
-        negreg = negnext;
-        negnext = negnext2;
+        if constexpr (!MULTI) {
+#pragma unroll
+            for (int k = 0; k < NN; ++k) ncur[k] = nnext[k];
+        }
+        nraw_ok = i + 2 < L;
+        tok_ahead = tok_ok ? tok_raw : -1;
         // Bounded staleness for L1-cached sample rows: refresh this SM's L1.
         if (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
             (threadIdx.x >> 5) == 0) {
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
     }
+    KB_T(8)
+    KB_T_DUMP
     // ContextRing::finish (trainer.cpp:71-75): residents in slot order.
+    const int i_end = Lmax;  // registers hold positions i_end-WF .. i_end+WF
     if (delta_wb) {
         // Deltas commute: no ordering to preserve.
-        const int i_end = Lmax;
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) {
             const int p = r < WF ? i_end - WF + r : i_end + 1 + (r - WF);
-            if (tok[r] >= 0) row_red_delta(syn0 + tok[r] * SM::STRIDE, ctx[r], entry + (p % C) * SM::STRIDE);
+            if (tok[r] >= 0) SL::red_delta(syn0 + tok[r] * STRIDE, ctx[r], ring + (p % C) * STRIDE);
         }
-        if (ttok >= 0) row_red_delta(syn0 + ttok * SM::STRIDE, tgt, entry + (i_end % C) * SM::STRIDE);
+        if (ttok >= 0) SL::red_delta(syn0 + ttok * STRIDE, tgt, ring + (i_end % C) * STRIDE);
     } else {
-        const int i_end = Lmax;  // registers hold positions i_end-WF .. i_end+WF
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) {
             const int p = r < WF ? i_end - WF + r : i_end + 1 + (r - WF);
-            if (tok[r] >= 0) Row2<H2>::store_shared(stash + (p % C) * SM::STRIDE, ctx[r]);
+            if (tok[r] >= 0) SL::store_shared(ring + (p % C) * STRIDE, ctx[r]);
         }
-        if (ttok >= 0) Row2<H2>::store_shared(stash + (i_end % C) * SM::STRIDE, tgt);
+        if (ttok >= 0) SL::store_shared(ring + (i_end % C) * STRIDE, tgt);
         const int first = max(0, tail);
         for (int s = 0; s < C; ++s) {
             // the resident position in slot s: first + ((s - first) mod C), if < L
             const int p = first + ((s - first % C) + C) % C;
             if (p < L) {
                 float2 v[H2];
-                Row2<H2>::load_shared(v, stash + s * SM::STRIDE);
-                Row2<H2>::store(syn0 + __ldg(ids + p) * SM::STRIDE, v);
+                SL::load_shared(v, ring + s * STRIDE);
+                SL::store(syn0 + __ldg(ids + p) * STRIDE, v);
             }
         }
     }
@@ -474,18 +625,18 @@ cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, 
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (resident != nullptr) return resident_sentences(kern, bytes, kK1Threads / LANES, resident);
+    constexpr int threads = K1sSmem<LANES, VEC, WF, NC>::THREADS;
+    if (resident != nullptr) return resident_sentences(kern, bytes, threads, threads / LANES, resident);
     if (blocks == 0) return cudaSuccess;
-    kern<<<blocks, kK1Threads, bytes, st>>>(m, b, n_neg, ctr);
+    kern<<<blocks, K1sSmem<LANES, VEC, WF, NC>::THREADS, bytes, st>>>(m, b, n_neg, ctr);
     return cudaGetLastError();
 }
 
 template <int LANES, int VEC, int WF, int NC>
 cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
                           cudaStream_t st, int* resident) {
-    constexpr int GPW = 32 / LANES;
-    const int warps = (b.n_sentences + GPW - 1) / GPW;
-    const int blocks = (warps * 32 + kK1Threads - 1) / kK1Threads;
+    constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;
+    const int blocks = (b.n_sentences + per_block - 1) / per_block;
     const bool multi = n_neg + 1 > NC;
     if (multi) {
         return fast ? launch_k1s_inst<LANES, VEC, WF, NC, true, true>(blocks, m, b, n_neg, ctr, st, resident)
@@ -511,9 +662,10 @@ cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, 
     }
 }
 
-#define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(32, 4) X(32, 8)
+#define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(16, 8) X(32, 4) X(32, 8)
 
 // Requires n_neg <= 2 * LANES (negatives are distributed two per lane).
+#ifndef FW2V_KBENCH  // tools/kbench.cu instantiates single kernels directly
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
                        DevCounters* ctr, cudaStream_t st, int* resident) {
 #define FW2V_CASE(L_, V_) \
@@ -530,5 +682,7 @@ bool k1s_supported(int lanes, int vec, int n_neg, int wf) {
 #undef FW2V_CASE
     return false;
 }
+
+#endif
 
 } // namespace fw2v

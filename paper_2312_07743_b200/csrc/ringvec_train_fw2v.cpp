@@ -105,6 +105,8 @@ TrainResult train(const Corpus& corpus, const TrainConfig& raw_config, TrainObse
     c.l1_refresh_log2 = env_int("FW2V_L1_REFRESH_LOG2", c.l1_refresh_log2);
     c.delta_writeback = env_int("FW2V_DELTA_WRITEBACK", c.delta_writeback);
     c.max_inflight = env_int("FW2V_MAX_INFLIGHT", c.max_inflight);
+    c.hot_rows = env_int("FW2V_HOT_ROWS", c.hot_rows);
+    c.hot_replicas = env_int("FW2V_HOT_REPLICAS", c.hot_replicas);
 
     std::vector<uint64_t> counts(static_cast<size_t>(vocab.size()));
     for (int32_t w = 0; w < vocab.size(); ++w) counts[static_cast<size_t>(w)] = vocab.entry(w).count;

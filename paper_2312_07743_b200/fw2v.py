@@ -65,6 +65,7 @@ class CConfig(C.Structure):
         ("device", C.c_int32), ("deterministic", C.c_int32), ("sampler", C.c_int32),
         ("fast_sigmoid", C.c_int32), ("k1_lanes", C.c_int32), ("streams", C.c_int32),
         ("l1_refresh_log2", C.c_int32), ("delta_writeback", C.c_int32), ("max_inflight", C.c_int32),
+        ("hot_rows", C.c_int32), ("hot_replicas", C.c_int32),
     ]
 
 
@@ -125,6 +126,8 @@ class TrainConfig:
     l1_refresh_log2: int = 5
     delta_writeback: bool = True
     max_inflight: int = 0
+    hot_rows: int = 64
+    hot_replicas: int = 16
 
     @property
     def context_width(self) -> int:

@@ -70,7 +70,7 @@ def test_train_deterministic_bitwise(oracle, dim, window, n_neg, sub):
     np.testing.assert_array_equal(go, ro)
 
 
-@pytest.mark.parametrize("dim,lanes", [(8, 0), (12, 0), (16, 0), (32, 0), (64, 0), (128, 0), (128, 16),
+@pytest.mark.parametrize("dim,lanes", [(8, 0), (12, 0), (16, 0), (32, 0), (64, 0), (128, 0), (128, 32), (128, 16),
                                        (128, 8), (256, 0), (300, 0), (512, 0)])
 @pytest.mark.parametrize("window", [2, 5, 7])
 @pytest.mark.parametrize("mode", ["lifetime", "window_snapshot"])
@@ -83,7 +83,8 @@ def test_k1_single_sentence_semantics(oracle, dim, lanes, window, mode):
     negs = fixed_negatives(int(offsets[-1]), n_neg, V, seed=9)
     alphas = np.full(len(offsets) - 1, 0.025, np.float32)
     cfg = dict(dim=dim, window=window, negatives=n_neg, workers=4, reuse_mode=mode)
-    gcfg = dict(cfg, deterministic=0, fast_sigmoid=False, k1_lanes=lanes, l1_refresh_log2=0, delta_writeback=False)
+    gcfg = dict(cfg, deterministic=0, fast_sigmoid=False, k1_lanes=lanes, l1_refresh_log2=0, delta_writeback=False,
+                hot_rows=0)
     ri, _ = oracle.init_model(V, dim, 5)
     ro = (ri[::-1] * 4.0).copy()
     gi0, go0 = ri.copy(), ro.copy()
@@ -158,3 +159,71 @@ def test_hogwild_uses_reference_batches(ref):
     assert rep.words_trained == rrep.words_trained
     assert rep.sentences_trained == rrep.sentences_trained
     assert rep.analytic == rrep.analytic
+
+
+def _disjoint_batch(n, L, pool, n_neg, seed, distinct=False):
+    """n sentences of length L whose ids and negatives come from disjoint
+    per-sentence token pools: Hogwild sentences never share a row. distinct:
+    no token repeats inside a sentence (pool >= L)."""
+    rng = np.random.default_rng(seed)
+    pick = (lambda k: rng.permutation(pool)[:k]) if distinct else (lambda k: rng.integers(0, pool, k))
+    ids = np.concatenate([s * pool + pick(L) for s in range(n)]).astype(np.int32)
+    negs = np.concatenate([s * pool + rng.integers(0, pool, L * n_neg) for s in range(n)]).astype(np.int32)
+    offsets = (np.arange(n + 1) * L).astype(np.uint64)
+    counts = (100 + n * pool - np.arange(n * pool)).astype(np.uint64)
+    return counts, offsets, ids, negs
+
+
+@pytest.mark.parametrize("dim", [16, 32, 64, 128, 256])
+@pytest.mark.parametrize("delta", [False, True])
+def test_k1s_disjoint_batch_equals_serial(oracle, dim, delta):
+    """A whole Hogwild K1s batch (several sentences per warp at small lane
+    counts) over row-disjoint sentences equals the reference snapshot order
+    applied sentence by sentence, up to FP association. Overwrite write-back:
+    duplicates inside a sentence included; delta write-back (red.add of the
+    ring rows' final - loaded) is exact when a sentence's ring never holds one
+    token twice."""
+    n, L, n_neg = 96, 40, 5
+    pool = 48 if delta else 12
+    counts, offsets, ids, negs = _disjoint_batch(n, L, pool, n_neg, seed=dim, distinct=delta)
+    V = len(counts)
+    alphas = np.full(n, 0.025, np.float32)
+    cfg = dict(dim=dim, window=5, negatives=n_neg, workers=4, reuse_mode="window_snapshot")
+    ri, _ = oracle.init_model(V, dim, 3)
+    ro = (ri[::-1] * 4.0).copy()
+    gi0, go0 = ri.copy(), ro.copy()
+    oracle.train_sentences(ri, ro, offsets, ids, negs, alphas, OConfig(**cfg))
+    with _trainer(counts=counts, deterministic=0, fast_sigmoid=False, hot_rows=0, l1_refresh_log2=0,
+                  delta_writeback=delta, **cfg) as t:
+        t.set_model(gi0, go0)
+        t.train_sentences(offsets, ids, negs, alphas, serial=False)
+        gi, go = t.get_model()
+    assert np.abs(gi - ri).max() <= 2e-5 * np.abs(ri).max() + 1e-7
+    assert np.abs(go - ro).max() <= 2e-5 * np.abs(ro).max() + 1e-7
+
+
+@pytest.mark.parametrize("replicas", [1, 2, 4])
+def test_k1s_hot_replicas_average(oracle, replicas):
+    """Hot-row replicas: rows < hot_rows are trained by sentence s on replica
+    s mod R and averaged after the pass. With one sentence, its replica holds
+    the reference update and the other R-1 replicas the untouched rows, so
+    hot output rows end at v0 + (v_ref - v0) / R; everything else is exact."""
+    dim, n_neg, hot = 128, 5, 20
+    counts, offsets, ids = random_corpus(1, 60, 40, seed=11, min_len=60)
+    V = len(counts)
+    negs = fixed_negatives(int(offsets[-1]), n_neg, V, seed=2)
+    alphas = np.full(1, 0.025, np.float32)
+    cfg = dict(dim=dim, window=5, negatives=n_neg, workers=4, reuse_mode="window_snapshot")
+    ri, _ = oracle.init_model(V, dim, 5)
+    ro = (ri[::-1] * 4.0).copy()
+    gi0, go0 = ri.copy(), ro.copy()
+    oracle.train_sentences(ri, ro, offsets, ids, negs, alphas, OConfig(**cfg))
+    with _trainer(counts=counts, deterministic=0, fast_sigmoid=False, l1_refresh_log2=0, delta_writeback=False,
+                  hot_rows=hot, hot_replicas=replicas, **cfg) as t:
+        t.set_model(gi0, go0)
+        t.train_sentences(offsets, ids, negs, alphas, serial=False)
+        gi, go = t.get_model()
+    want = ro.copy()
+    want[:hot] = go0[:hot] + (ro[:hot] - go0[:hot]) / replicas
+    assert np.abs(gi - ri).max() <= 2e-5 * np.abs(ri).max() + 1e-7
+    assert np.abs(go - want).max() <= 2e-5 * np.abs(ro).max() + 1e-7

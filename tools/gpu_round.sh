@@ -16,3 +16,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1s 
   python tools/ncu_probe.py window_snapshot 20000 128 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -3 gpurun_out/ncu_full_$TAG.log
 ls -la gpurun_out
+if [ -n "$EXTRA" ]; then
+  for a in $EXTRA; do
+    timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 20 ${a//,/ } 2>&1 | python -c "import sys,json; j=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$a', round(j['value']/1e6,1), 'Mw/s')"
+  done
+fi

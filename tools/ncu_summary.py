@@ -101,7 +101,8 @@ def main():
         "dram_bytes_per_launch": (rd or 0) + (wr or 0),
         "registers_per_thread": num("launch__registers_per_thread"),
         "grid": d.get("Grid Size"),
-        "note": "one launch = one producer batch (~1045 sentences, ~619k trained words) of the text8-shaped epoch",
+        "note": "one launch = the whole text8-shaped epoch as one batch (tools/ncu_probe.py window_snapshot 20000 128 1: 16,719 sentences, 9.9M trained words)",
+        "words_per_launch": 9897591,
     }
     with open(os.path.join(out_dir, "ncu_k1s_summary.json"), "w") as f:
         json.dump(summary, f, indent=1)
