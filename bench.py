@@ -242,7 +242,7 @@ def run_ours(args, world, rank, local, dist):
         ecfg = fw.TrainConfig(**{**cfg.__dict__, "epochs": 1})
         with fw.Trainer(ecfg, corpus.counts) as et:
             et.train_corpus(corpus)  # warm-up epoch (allocates pinned buffers)
-            e_words, e_secs, h2d = 0, 0.0, 0
+            e_words, e_secs, h2d, bwps = 0, 0.0, 0, 0.0
             for _ in range(max(1, min(args.steps, 3))):
                 if dist is not None:
                     dist.barrier()
@@ -250,6 +250,7 @@ def run_ours(args, world, rank, local, dist):
                 e_words += rep.words_trained
                 e_secs += rep.wall_seconds
                 h2d = rep.h2d_bytes
+                bwps = rep.batching_words_per_sec
             e_rate = e_words / e_secs
             if dist is not None:
                 t = torch.tensor([e_secs], device=f"cuda:{local}", dtype=torch.float64)
@@ -257,7 +258,8 @@ def run_ours(args, world, rank, local, dist):
                 e_rate = e_words * world / float(t.item())
             e2e = {"value": e_rate, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                    "d2h_bytes_per_step": 64 * args.streams,
-                   "path": "fw2v_train_corpus (C-ABI): host batching threads -> pinned -> H2D -> K1s"}
+                   "path": "fw2v_train_corpus (C-ABI): host batching threads -> pinned -> H2D -> K1s",
+                   "host_batching_words_per_sec_per_thread": bwps, "batching_threads": args.streams}
 
     peak, peak_src = load_peaks()
     bpw = algorithmic_bytes_per_word(args.dim, args.negatives)
@@ -330,7 +332,7 @@ def main():
     ap.add_argument("--batch-sentences", type=int, default=10000)
     ap.add_argument("--streams", type=int, default=16)
     ap.add_argument("--reuse-mode", default="window_snapshot")
-    ap.add_argument("--sampler", default="reference", choices=["reference", "alias"])
+    ap.add_argument("--sampler", default="alias", choices=["reference", "alias"])
     ap.add_argument("--l1-refresh-log2", type=int, default=5)
     ap.add_argument("--ref-sentences", type=int, default=4000)
     ap.add_argument("--no-e2e", action="store_true")

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <ctime>
+#include <sys/mman.h>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -163,8 +164,11 @@ void build_table(const uint64_t* counts, int32_t v, double power, uint64_t size,
 // "unigram^0.75 alias table"): one 64-bit draw -> column (Lemire
 // multiply-high) + 32-bit coin.
 struct AliasTable {
-    std::vector<uint32_t> prob;  // threshold in 2^32 units
-    std::vector<int32_t> alias;
+    struct Entry {
+        uint32_t prob;  // threshold in 2^32 units
+        int32_t alias;
+    };
+    std::vector<Entry> e;  // one 8-byte entry per column: one cache access per draw
     uint32_t n = 0;
     void build(const uint64_t* counts, int32_t v, double power) {
         n = static_cast<uint32_t>(v);
@@ -176,15 +180,13 @@ struct AliasTable {
             p[static_cast<size_t>(w)] *= static_cast<double>(v) / total;
             (p[static_cast<size_t>(w)] < 1.0 ? small : large).push_back(w);
         }
-        prob.assign(static_cast<size_t>(v), 0xffffffffu);
-        alias.resize(static_cast<size_t>(v));
-        for (int32_t w = 0; w < v; ++w) alias[static_cast<size_t>(w)] = w;
+        e.resize(static_cast<size_t>(v));
+        for (int32_t w = 0; w < v; ++w) e[static_cast<size_t>(w)] = Entry{0xffffffffu, w};
         while (!small.empty() && !large.empty()) {
             const int32_t s = small.back(), l = large.back();
             small.pop_back();
             const double ps = p[static_cast<size_t>(s)];
-            prob[static_cast<size_t>(s)] = static_cast<uint32_t>(std::min(4294967295.0, ps * 4294967296.0));
-            alias[static_cast<size_t>(s)] = l;
+            e[static_cast<size_t>(s)] = Entry{static_cast<uint32_t>(std::min(4294967295.0, ps * 4294967296.0)), l};
             p[static_cast<size_t>(l)] -= 1.0 - ps;
             if (p[static_cast<size_t>(l)] < 1.0) {
                 large.pop_back();
@@ -194,7 +196,8 @@ struct AliasTable {
     }
     inline int32_t sample(uint64_t u) const {
         const uint32_t col = static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(u)) * n) >> 32);
-        return static_cast<uint32_t>(u >> 32) < prob[col] ? static_cast<int32_t>(col) : alias[col];
+        const Entry& x = e.data()[col];
+        return static_cast<uint32_t>(u >> 32) < x.prob ? static_cast<int32_t>(col) : x.alias;
     }
 };
 
@@ -239,10 +242,59 @@ struct CorpusView {
     uint64_t n;
 };
 
+// Host array on 2 MB pages (transparent huge pages via madvise): the 40 MB
+// negative table is read at random, and with 4 KB pages nearly every draw
+// would also miss the TLB.
+template <typename T>
+class HugeArray {
+  public:
+    HugeArray() = default;
+    HugeArray(const HugeArray&) = delete;
+    HugeArray& operator=(const HugeArray&) = delete;
+    ~HugeArray() { release(); }
+    void resize(size_t n) {
+        release();
+        n_ = n;
+        bytes_ = ((n * sizeof(T) + kPage - 1) / kPage) * kPage;
+        if (bytes_ == 0) return;
+        void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) throw std::bad_alloc();
+        madvise(p, bytes_, MADV_HUGEPAGE);
+        p_ = static_cast<T*>(p);
+    }
+    T* data() { return p_; }
+    const T* data() const { return p_; }
+    size_t size() const { return n_; }
+
+  private:
+    static constexpr size_t kPage = size_t{2} << 20;
+    void release() {
+        if (p_ != nullptr) munmap(p_, bytes_);
+        p_ = nullptr;
+        n_ = bytes_ = 0;
+    }
+    T* p_ = nullptr;
+    size_t n_ = 0, bytes_ = 0;
+};
+
+// x % d for a fixed d >= 1 without a 64-bit divide: q = floor(x * floor(2^64/d) / 2^64)
+// is q_true or q_true - 1, so one conditional subtract makes it exact.
+struct FastMod {
+    uint64_t d = 1, inv = 0;
+    explicit FastMod(uint64_t d_ = 1) : d(d_), inv(d_ > 1 ? ~uint64_t{0} / d_ : 0) {}
+    inline uint64_t operator()(uint64_t x) const {
+        if (d == 1) return 0;
+        const uint64_t q = static_cast<uint64_t>((static_cast<unsigned __int128>(x) * inv) >> 64);
+        uint64_t r = x - q * d;
+        return r >= d ? r - d : r;
+    }
+};
+
 struct Sampler {
     const double* keep = nullptr;     // null: subsampling off
     const int32_t* slots = nullptr;   // reference table
     uint64_t table_size = 0;
+    FastMod mod{1};
     const AliasTable* alias = nullptr;  // non-null: alias sampler
     int n_neg = 0;
 };
@@ -268,10 +320,16 @@ uint64_t assemble(const CorpusView& c, uint64_t& cursor, uint64_t end, uint64_t 
         if (w + (e - b) > out.cap_words) break;  // caller sized for the worst case; never hit
         const uint64_t start = w;
         if (sp.keep != nullptr) {
+            // One next_double per raw token, kept in order (corpus.cpp:232-241);
+            // branch-free: keep decisions are coin flips for frequent words.
+            int32_t* dst = out.ids + w;
+            uint64_t n = 0;
             for (uint64_t p = b; p < e; ++p) {
                 const int32_t id = c.ids[p];
-                if (rng.next_double() < sp.keep[id]) out.ids[w++] = id;
+                dst[n] = id;
+                n += rng.next_double() < sp.keep[id] ? 1 : 0;
             }
+            w += n;
         } else {
             std::memcpy(out.ids + w, c.ids + b, sizeof(int32_t) * (e - b));
             w += e - b;
@@ -280,12 +338,38 @@ uint64_t assemble(const CorpusView& c, uint64_t& cursor, uint64_t end, uint64_t 
         if (w == start) continue;
         int32_t* ng = out.negs + start * static_cast<uint64_t>(n_neg);
         const uint64_t cnt = (w - start) * static_cast<uint64_t>(n_neg);
+        // The stream state and tables live in locals: through the references the
+        // compiler must assume the int32 stores into ng may alias them.
+        Rng r = rng;
         if (sp.alias != nullptr) {
-            for (uint64_t x = 0; x < cnt; ++x) ng[x] = sp.alias->sample(rng.next());
+            const AliasTable::Entry* const E = sp.alias->e.data();
+            const uint64_t n = sp.alias->n;
+            for (uint64_t x = 0; x < cnt; ++x) {
+                const uint64_t u = r.next();
+                const uint32_t col = static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(u)) * n) >> 32);
+                const AliasTable::Entry en = E[col];
+                // branch-free select (acceptance is a coin flip for most columns)
+                const int32_t m = -static_cast<int32_t>(static_cast<uint32_t>(u >> 32) < en.prob);
+                ng[x] = (static_cast<int32_t>(col) & m) | (en.alias & ~m);
+            }
         } else {
-            const uint64_t ts = sp.table_size;
-            for (uint64_t x = 0; x < cnt; ++x) ng[x] = sp.slots[rng.next() % ts];
+            // Same draws in the same order as slots[rng.next() % size] (sampler.cpp:37-39);
+            // the table (40 MB at 1e7 slots) is gathered 64 draws at a time with
+            // prefetches so the cache misses overlap.
+            constexpr uint64_t kG = 64;
+            uint64_t idx[kG];
+            const FastMod mod = sp.mod;
+            const int32_t* const slots = sp.slots;
+            for (uint64_t x0 = 0; x0 < cnt; x0 += kG) {
+                const uint64_t g = std::min(kG, cnt - x0);
+                for (uint64_t j = 0; j < g; ++j) {
+                    idx[j] = mod(r.next());
+                    __builtin_prefetch(slots + idx[j], 0, 3);
+                }
+                for (uint64_t j = 0; j < g; ++j) ng[x0 + j] = slots[idx[j]];
+            }
         }
+        rng = r;
         ++kept;
         out.offsets[kept] = static_cast<uint32_t>(w);
     }
@@ -404,7 +488,7 @@ struct fw2v_ctx {
     uint64_t total_retained = 0;
     std::vector<double> keep;
     bool keep_on = false;
-    std::vector<int32_t> slots;
+    HugeArray<int32_t> slots;  // reference negative table (sampler.cpp:9-35)
     AliasTable alias;
     float* syn0 = nullptr;
     float* syn1 = nullptr;
@@ -429,6 +513,7 @@ struct fw2v_ctx {
         } else {
             s.slots = slots.data();
             s.table_size = slots.size();
+            s.mod = FastMod(slots.size());
         }
         return s;
     }
@@ -827,6 +912,10 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
             cap_s = std::max(cap_s, s);
         }
         x->ensure_lanes(P, cap_w, cap_s);
+        // Sub-batch size: a quarter of a producer's chunk (at least 256 sentences,
+        // enough to keep the device full across the streams), never above S.
+        const uint64_t sub = x->deterministic ? cfg.batch_sentences
+                                              : std::min<uint64_t>(cfg.batch_sentences, std::max<uint64_t>(256, chunk / 4));
         const uint64_t schedule_total =
             cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
         const Sampler sp = x->sampler();
@@ -871,14 +960,25 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                         uint64_t wsum = 0;
                         uint64_t* an = &an_acc[static_cast<size_t>(p) * 5];
                         int which = 0;
-                        for (uint64_t k = 0; cursor < end; ++k) {
+                        // Batch k (reference stream derive(seed, epoch, p, k), S kept
+                        // sentences) is shipped in sub-batches of `sub` sentences drawn
+                        // from the same stream in the same order, so the kernels of one
+                        // sub-batch overlap the host assembly of the next.
+                        Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), 0);
+                        uint64_t k = 0, left = cfg.batch_sentences;
+                        while (cursor < end) {
+                            if (left == 0) {
+                                ++k;
+                                left = cfg.batch_sentences;
+                                rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), k);
+                            }
                             Slot& sl = ln.slot[which];
                             if (sl.in_flight) FW2V_CK(cudaEventSynchronize(sl.h2d_done));
-                            Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), k);
                             const double c0 = thread_cpu_seconds();
                             uint64_t words = 0;
                             const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
-                            const uint64_t kept = assemble(corpus, cursor, end, cfg.batch_sentences, sp, rng, bo, &words);
+                            const uint64_t kept = assemble(corpus, cursor, end, std::min(left, sub), sp, rng, bo, &words);
+                            left -= kept;
                             // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
                             const uint64_t base = reserved.fetch_add(words);
                             for (uint64_t q = 0; q < kept; ++q) sl.h_alpha[q] = lr_at(base + sl.h_off[q], schedule_total, cfg.alpha0);
@@ -1134,7 +1234,8 @@ int64_t fw2v_assemble_batch(const uint64_t* counts, int32_t vocab_size, const ui
     int rc = guarded([&] {
         if (max_sentences < 1) fail(FW2V_ERR_BAD_ARGUMENT, "batch size must be >= 1");
         if (negatives < 0) fail(FW2V_ERR_BAD_ARGUMENT, "negatives must be >= 0");
-        std::vector<int32_t> slots(table_size);
+        HugeArray<int32_t> slots;
+        slots.resize(table_size);
         build_table(counts, vocab_size, power, table_size, slots.data());
         std::vector<double> keep(static_cast<size_t>(vocab_size));
         const bool on = keep_probs(counts, vocab_size, threshold, keep.data());
@@ -1142,6 +1243,7 @@ int64_t fw2v_assemble_batch(const uint64_t* counts, int32_t vocab_size, const ui
         sp.keep = on ? keep.data() : nullptr;
         sp.slots = slots.data();
         sp.table_size = table_size;
+        sp.mod = FastMod(table_size);
         sp.n_neg = negatives;
         const uint64_t total = offsets[n_sentences] - offsets[0];
         std::vector<uint32_t> off(n_sentences + 1);
