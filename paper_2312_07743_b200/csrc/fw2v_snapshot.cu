@@ -88,14 +88,6 @@ struct Butterfly {
     }
 };
 
-__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16_ca(float* smem, const float* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -123,51 +115,108 @@ struct K1sSmem {
     static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
 };
 
-// A lane's slice of a row: VEC = 2*H2 columns as H2/2 16-byte chunks spaced CS
-// floats apart (chunk c of lane l at column 4*(c*LANES + l), CS = 4*LANES), so
-// one 16-byte access by a lane group covers a contiguous 16*LANES-byte span:
+// A lane's slice of a row: VEC = 2*H2 columns as chunks of CW floats (16 bytes
+// when H2 is even, else 8 bytes, e.g. d=300 on 32 lanes x 10 columns) spaced
+// CS = CW*LANES floats apart (chunk c of lane l at column CW*(c*LANES + l)), so
+// one chunk access by a lane group covers a contiguous CW*4*LANES-byte span:
 // coalesced in HBM/L2 and bank-conflict free in shared memory.
-template <int H2, int CS>
+template <int H2, int LANES>
 struct Slice {
-    static_assert(H2 % 2 == 0, "16-byte chunks");
-    static constexpr int NCH = H2 / 2;
-    __device__ __forceinline__ static void set(float2 (&v)[H2], int c, float4 t) {
-        v[2 * c] = make_float2(t.x, t.y);
-        v[2 * c + 1] = make_float2(t.z, t.w);
-    }
-    __device__ __forceinline__ static float4 get(const float2 (&v)[H2], int c) {
-        return make_float4(v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
-    }
+    static constexpr int CW = H2 % 2 == 0 ? 4 : 2;
+    static constexpr int CS = CW * LANES;
+    static constexpr int NCH = 2 * H2 / CW;
+    __device__ __forceinline__ static const float* chunk(const float* p, int c) { return p + c * CS; }
     __device__ __forceinline__ static void load(float2 (&v)[H2], const float* p) {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) set(v, c, __ldcg(reinterpret_cast<const float4*>(p + c * CS)));
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (CW == 4) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(p + c * CS));
+                v[2 * c] = make_float2(t.x, t.y);
+                v[2 * c + 1] = make_float2(t.z, t.w);
+            } else {
+                v[c] = __ldcg(reinterpret_cast<const float2*>(p + c * CS));
+            }
+        }
     }
     __device__ __forceinline__ static void load_early(float2 (&v)[H2], const float* p) {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) set(v, c, ldcg_early(p + c * CS));
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (CW == 4) {
+                const float4 t = ldcg_early(p + c * CS);
+                v[2 * c] = make_float2(t.x, t.y);
+                v[2 * c + 1] = make_float2(t.z, t.w);
+            } else {
+                asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v[c].x), "=f"(v[c].y) : "l"(p + c * CS));
+            }
+        }
     }
     __device__ __forceinline__ static void store(float* p, const float2 (&v)[H2]) {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) __stcg(reinterpret_cast<float4*>(p + c * CS), get(v, c));
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (CW == 4)
+                __stcg(reinterpret_cast<float4*>(p + c * CS), make_float4(v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y));
+            else
+                __stcg(reinterpret_cast<float2*>(p + c * CS), v[c]);
+        }
     }
     __device__ __forceinline__ static void load_shared(float2 (&v)[H2], const float* p) {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) set(v, c, *reinterpret_cast<const float4*>(p + c * CS));
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (CW == 4) {
+                const float4 t = *reinterpret_cast<const float4*>(p + c * CS);
+                v[2 * c] = make_float2(t.x, t.y);
+                v[2 * c + 1] = make_float2(t.z, t.w);
+            } else {
+                v[c] = *reinterpret_cast<const float2*>(p + c * CS);
+            }
+        }
     }
     __device__ __forceinline__ static void store_shared(float* p, const float2 (&v)[H2]) {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) *reinterpret_cast<float4*>(p + c * CS) = get(v, c);
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (CW == 4)
+                *reinterpret_cast<float4*>(p + c * CS) = make_float4(v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
+            else
+                *reinterpret_cast<float2*>(p + c * CS) = v[c];
+        }
+    }
+    __device__ __forceinline__ static void zero_shared(float* p) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (CW == 4) *reinterpret_cast<float4*>(p + c * CS) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            else *reinterpret_cast<float2*>(p + c * CS) = make_float2(0.0f, 0.0f);
+        }
+    }
+    // Stage the lane's slice of a global row into shared memory (cp.async, L2 or L1).
+    __device__ __forceinline__ static void stage(float* dst, const float* src, bool via_l1) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + c * CS));
+            if constexpr (CW == 4) {
+                if (via_l1) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
+                else asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
+            } else {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + c * CS) : "memory");
+            }
+        }
     }
     // row += d at L2 when pred (no branch).
     __device__ __forceinline__ static void red_add_if(bool pred, float* p, const float2 (&d)[H2]) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            const float4 t = get(d, c);
-            asm volatile(
-                "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-                "@q red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p + c * CS),
-                "f"(t.x), "f"(t.y), "f"(t.z), "f"(t.w), "r"(static_cast<int>(pred))
-                : "memory");
+            if constexpr (CW == 4) {
+                asm volatile(
+                    "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+                    "@q red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p + c * CS),
+                    "f"(d[2 * c].x), "f"(d[2 * c].y), "f"(d[2 * c + 1].x), "f"(d[2 * c + 1].y), "r"(static_cast<int>(pred))
+                    : "memory");
+            } else {
+                asm volatile(
+                    "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+                    "@q red.global.add.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p + c * CS),
+                    "f"(d[c].x), "f"(d[c].y), "r"(static_cast<int>(pred))
+                    : "memory");
+            }
         }
     }
     // row += (v - entry): the ring row's accumulated update since it was loaded.
@@ -183,7 +232,7 @@ struct Slice {
 template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
 __global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC>::THREADS, K1sSmem<LANES, VEC, WF, NC>::MINB)
 k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) {
-    static_assert(VEC % 4 == 0, "K1s stages 16-byte slices");
+    static_assert(VEC % 2 == 0, "K1s stages 8- or 16-byte chunks");
     using SM = K1sSmem<LANES, VEC, WF, NC>;
     constexpr int NCTX = SM::NCTX;
     constexpr int C = SM::C;
@@ -199,7 +248,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     // lanes of the upper half load those two sample rows in swapped order, so
     // that level needs no selects.
     constexpr bool kPreswap = NC % 2 == 0;
-    using SL = Slice<H2, 4 * LANES>;
+    using SL = Slice<H2, LANES>;
     using BF = Butterfly<LANES / 2, NV>;
     constexpr int NF = BF::final_count();
     static_assert(NV <= 255 && NC <= 16 && NCTX <= 16, "slot words");
@@ -211,8 +260,8 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     const int sent = static_cast<int>((blockIdx.x * SM::THREADS + threadIdx.x) / LANES);
     const bool has = sent < b.n_sentences;
     float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
-    float* sbuf = gsh + SM::GPAD + sub * 4;                  // + (parity*NC + q)*STRIDE
-    float* ring = gsh + SM::GPAD + 2 * NC * STRIDE + sub * 4;  // + slot*STRIDE
+    float* sbuf = gsh + SM::GPAD + sub * SL::CW;                  // + (parity*NC + q)*STRIDE
+    float* ring = gsh + SM::GPAD + 2 * NC * STRIDE + sub * SL::CW;  // + slot*STRIDE
     const bool delta_wb = (m.flags & kFlagDeltaRing) != 0;
 
     uint32_t beg = 0, len = 0;
@@ -229,10 +278,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     const int32_t* __restrict__ ids = b.ids + beg;
     const int32_t* __restrict__ negs = b.negs + static_cast<size_t>(beg) * n_neg;
     // Row offsets use the compile-time stride (host checks |V| * stride < 2^31).
-    float* __restrict__ syn0 = m.syn0 + sub * 4;
-    float* __restrict__ syn1 = m.syn1 + sub * 4;
+    float* __restrict__ syn0 = m.syn0 + sub * SL::CW;
+    float* __restrict__ syn1 = m.syn1 + sub * SL::CW;
     // Output row of sample s >= 0: hot rows go to this sentence's replica.
-    float* const hot_base = m.hot_k > 0 ? m.hot + (sent % m.hot_r) * m.hot_k * STRIDE + sub * 4 : syn1;
+    float* const hot_base = m.hot_k > 0 ? m.hot + (sent % m.hot_r) * m.hot_k * STRIDE + sub * SL::CW : syn1;
     const int hot_k = m.hot_k;
     auto srow = [&](int s) { return (s < hot_k ? hot_base : syn1) + s * STRIDE; };
     const int tail = L - C;  // positions >= tail stay resident until finish()
@@ -290,11 +339,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     for (int q = 0; q < (kMatch ? 1 : NC); ++q) psid[q] = -100;
 
     {
-        const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
         for (int q = 0; q < 2 * NC; ++q)
 #pragma unroll
-            for (int e = 0; e < VEC / 4; ++e) *reinterpret_cast<float4*>(sbuf + q * STRIDE + e * 4 * LANES) = z;
+            SL::zero_shared(sbuf + q * STRIDE);
     }
     const bool l1_samples = (m.flags & kFlagL1Samples) != 0;
     auto prefetch = [&](int target, const int (&nv)[MULTI ? 1 : NN], bool active, int parity) {
@@ -304,10 +352,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             const int s = q == 0 ? target : nv[q > 0 ? q - 1 : 0];
             if (active && q <= n_neg && s >= 0) {
 #pragma unroll
-                for (int e = 0; e < VEC / 4 * 4 * LANES; e += 4 * LANES) {
-                    if (l1_samples) cp_async16_ca(dst + q * STRIDE + e, srow(s) + e);
-                    else cp_async16(dst + q * STRIDE + e, srow(s) + e);
-                }
+                SL::stage(dst + q * STRIDE, srow(s), l1_samples);
             }
         }
     };
@@ -662,7 +707,7 @@ cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, 
     }
 }
 
-#define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(16, 8) X(32, 4) X(32, 8)
+#define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(16, 8) X(32, 4) X(32, 6) X(32, 8) X(32, 10) X(32, 12)
 
 // Requires n_neg <= 2 * LANES (negatives are distributed two per lane).
 #ifndef FW2V_KBENCH  // tools/kbench.cu instantiates single kernels directly

@@ -174,7 +174,7 @@ def _disjoint_batch(n, L, pool, n_neg, seed, distinct=False):
     return counts, offsets, ids, negs
 
 
-@pytest.mark.parametrize("dim", [16, 32, 64, 128, 256])
+@pytest.mark.parametrize("dim", [16, 32, 64, 128, 256, 300])
 @pytest.mark.parametrize("delta", [False, True])
 def test_k1s_disjoint_batch_equals_serial(oracle, dim, delta):
     """A whole Hogwild K1s batch (several sentences per warp at small lane
