@@ -179,7 +179,8 @@ def run_ours(args, world, rank, local, dist):
     shape = fw.TEXT8_SHAPE if args.workload == "text8" else fw.ONEBW_SHAPE
     corpus = fw.synth_zipf(**shape)
     cfg = fw.TrainConfig(dim=args.dim, window=args.window, negatives=args.negatives, epochs=max(1, args.steps),
-                         workers=args.streams, batch_sentences=args.batch_sentences, subsample=1e-4,
+                         workers=args.chunks, streams=args.streams, batch_sentences=args.batch_sentences,
+                         subsample=1e-4,
                          seed=1 + rank, deterministic=0, reuse_mode=args.reuse_mode, device=local,
                          sampler=args.sampler, l1_refresh_log2=args.l1_refresh_log2)
     trainer = fw.Trainer(cfg, corpus.counts)
@@ -283,7 +284,7 @@ def run_ours(args, world, rank, local, dist):
                                    f"{shape['tokens']} tokens, 1000-token sentences), 1 epoch per step",
                        "dim": args.dim, "window": args.window, "negatives": args.negatives, "subsample": 1e-4,
                        "words_per_step_per_gpu": words_per_step, "batch_sentences": args.batch_sentences,
-                       "streams": args.streams, "reuse_mode": args.reuse_mode,
+                       "streams": args.streams, "chunks": args.chunks, "reuse_mode": args.reuse_mode,
                        "kernel": "K1s (FULL-W2V independent negatives, Hogwild)", "sampler": args.sampler,
                        "l1_refresh_log2": args.l1_refresh_log2,
                        "parallelism": f"dp{world} replicas + NCCL avg per step" if world > 1 else "single GPU",
@@ -330,7 +331,9 @@ def main():
     ap.add_argument("--window", type=int, default=5)
     ap.add_argument("--negatives", type=int, default=5)
     ap.add_argument("--batch-sentences", type=int, default=10000)
-    ap.add_argument("--streams", type=int, default=16)
+    ap.add_argument("--streams", type=int, default=16, help="batching threads = CUDA streams")
+    ap.add_argument("--chunks", type=int, default=64,
+                    help="corpus chunks (TrainConfig.workers: the reference's producer partition and RNG streams)")
     ap.add_argument("--reuse-mode", default="window_snapshot")
     ap.add_argument("--sampler", default="alias", choices=["reference", "alias"])
     ap.add_argument("--l1-refresh-log2", type=int, default=5)

@@ -519,14 +519,16 @@ struct fw2v_ctx {
         return s;
     }
 
+    // The corpus is cut into `workers` contiguous chunks (the reference's
+    // producer partition, trainer.cpp:431-434; chunk p, batch k uses the stream
+    // derive(seed, epoch, p, k)); `streams` batching threads, one CUDA stream
+    // each, pull whole chunks from a shared counter (load balance across
+    // uneven host cores). streams = 0: one thread per chunk.
+    int chunks() const { return deterministic ? 1 : std::max(1, cfg.workers); }
     int producers() const {
         if (deterministic) return 1;
-        int p = cfg.streams > 0 ? cfg.streams : cfg.workers;
-        if (p <= 0) {
-            unsigned hw = std::thread::hardware_concurrency();
-            p = hw == 0 ? 1 : static_cast<int>(hw);
-        }
-        return p;
+        const int t = cfg.streams > 0 ? cfg.streams : cfg.workers;
+        return std::max(1, std::min(t, chunks()));
     }
 
     // Hogwild sentences in flight per stream (0 = no cap): a batch larger than
@@ -901,10 +903,11 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
         FW2V_CK(cudaSetDevice(x->cfg.device));
         const fw2v_config& cfg = x->cfg;
         const CorpusView corpus{offsets, ids, n_sentences};
-        const int P = x->producers();
-        const uint64_t chunk = (n_sentences + P - 1) / std::max(P, 1);  // trainer.cpp:431-434
+        const int P = x->producers();  // batching threads = CUDA streams
+        const int NC = x->chunks();
+        const uint64_t chunk = (n_sentences + NC - 1) / std::max(NC, 1);  // trainer.cpp:431-434
         uint64_t cap_w = 1, cap_s = 1;
-        for (int p = 0; p < P; ++p) {
+        for (int p = 0; p < NC; ++p) {
             const uint64_t b = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
             const uint64_t e = std::min(n_sentences, b + chunk);
             uint64_t w, s;
@@ -913,10 +916,11 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
             cap_s = std::max(cap_s, s);
         }
         x->ensure_lanes(P, cap_w, cap_s);
-        // Sub-batch size: a quarter of a producer's chunk (at least 256 sentences,
-        // enough to keep the device full across the streams), never above S.
+        // Sub-batches of ~256-511 sentences (equal parts of a chunk; enough to keep
+        // the device full across the streams), never above S.
+        const uint64_t parts = std::max<uint64_t>(1, chunk / 256);
         const uint64_t sub = x->deterministic ? cfg.batch_sentences
-                                              : std::min<uint64_t>(cfg.batch_sentences, std::max<uint64_t>(256, chunk / 4));
+                                              : std::min<uint64_t>(cfg.batch_sentences, (chunk + parts - 1) / parts);
         const uint64_t schedule_total =
             cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
         const Sampler sp = x->sampler();
@@ -945,22 +949,39 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                 for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, synced, 0));
             }
             std::atomic<uint64_t> reserved{x->words_trained};
+            // FW2V_TRACE=1: per sub-batch host and device timeline on stderr (diagnostics).
+            struct TraceRec {
+                int p;
+                double t0, t1, t2;
+                cudaEvent_t k0, k1;
+                uint64_t words;
+            };
+            static const bool trace = std::getenv("FW2V_TRACE") != nullptr;
+            std::vector<std::vector<TraceRec>> tr(static_cast<size_t>(P));
+            cudaEvent_t ev0 = nullptr;
+            if (trace) {
+                FW2V_CK(cudaEventCreate(&ev0));
+                FW2V_CK(cudaEventRecord(ev0, x->lanes[0].stream));
+                FW2V_CK(cudaEventSynchronize(ev0));
+            }
             std::vector<uint64_t> an_acc(static_cast<size_t>(P) * 5, 0);
             std::vector<std::string> errors(static_cast<size_t>(P));
             const double t0 = wall_seconds();
             std::vector<std::thread> threads;
-            for (int p = 0; p < P; ++p) {
-                threads.emplace_back([&, p] {
+            std::atomic<int> next_chunk{0};
+            for (int th = 0; th < P; ++th) {
+                threads.emplace_back([&, th] {
                     try {
                         FW2V_CK(cudaSetDevice(cfg.device));
-                        Lane& ln = x->lanes[static_cast<size_t>(p)];
+                        Lane& ln = x->lanes[static_cast<size_t>(th)];
+                        double cpu = 0.0;
+                        uint64_t wsum = 0;
+                        uint64_t* an = &an_acc[static_cast<size_t>(th) * 5];
+                        int which = 0;
+                        for (int p = next_chunk.fetch_add(1); p < NC; p = next_chunk.fetch_add(1)) {
                         const uint64_t begin = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
                         const uint64_t end = std::min(n_sentences, begin + chunk);
                         uint64_t cursor = begin;
-                        double cpu = 0.0;
-                        uint64_t wsum = 0;
-                        uint64_t* an = &an_acc[static_cast<size_t>(p) * 5];
-                        int which = 0;
                         // Batch k (reference stream derive(seed, epoch, p, k), S kept
                         // sentences) is shipped in sub-batches of `sub` sentences drawn
                         // from the same stream in the same order, so the kernels of one
@@ -976,9 +997,12 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                             Slot& sl = ln.slot[which];
                             if (sl.in_flight) FW2V_CK(cudaEventSynchronize(sl.h2d_done));
                             const double c0 = thread_cpu_seconds();
+                            const double w0 = trace ? wall_seconds() : 0.0;
                             uint64_t words = 0;
                             const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
-                            const uint64_t kept = assemble(corpus, cursor, end, std::min(left, sub), sp, rng, bo, &words);
+                            // A short first sub-batch per thread gets the device busy early.
+                            const uint64_t want = std::min(left, which == 0 && wsum == 0 && !x->deterministic ? std::min<uint64_t>(sub, 64) : sub);
+                            const uint64_t kept = assemble(corpus, cursor, end, want, sp, rng, bo, &words);
                             left -= kept;
                             // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
                             const uint64_t base = reserved.fetch_add(words);
@@ -1006,13 +1030,27 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                             sl.in_flight = true;
                             h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
                             const BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
+                            TraceRec rec{};
+                            if (trace) {
+                                rec = TraceRec{th, w0 - t0, 0.0, 0.0, nullptr, nullptr, words};
+                                rec.t1 = wall_seconds() - t0;
+                                FW2V_CK(cudaEventCreate(&rec.k0));
+                                FW2V_CK(cudaEventCreate(&rec.k1));
+                                FW2V_CK(cudaEventRecord(rec.k0, st));
+                            }
                             FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, P));
+                            if (trace) {
+                                FW2V_CK(cudaEventRecord(rec.k1, st));
+                                rec.t2 = wall_seconds() - t0;
+                                tr[static_cast<size_t>(th)].push_back(rec);
+                            }
                             which ^= 1;
                         }
+                        }  // chunks
                         batch_words.fetch_add(wsum);
                         batch_nanos.fetch_add(static_cast<uint64_t>(cpu * 1e9));
                     } catch (const Failure& f) {
-                        errors[static_cast<size_t>(p)] = f.msg;
+                        errors[static_cast<size_t>(th)] = f.msg;
                     }
                 });
             }
@@ -1021,6 +1059,21 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
             if (!x->deterministic && x->hot_k > 0) {
                 x->hot_sync(true, x->lanes[0].stream);
                 FW2V_CK(cudaStreamSynchronize(x->lanes[0].stream));
+            }
+            if (trace) {
+                std::fprintf(stderr, "[fw2v trace] epoch %d wall %.3f ms (host: asm start/end, launch; device: kernel start/end ms)\n",
+                             epoch, 1e3 * (wall_seconds() - t0));
+                for (auto& lane_tr : tr)
+                    for (TraceRec& r : lane_tr) {
+                        float a = 0.0f, b = 0.0f;
+                        cudaEventElapsedTime(&a, ev0, r.k0);
+                        cudaEventElapsedTime(&b, ev0, r.k1);
+                        std::fprintf(stderr, "[fw2v trace] p%02d words %7llu host %.3f %.3f %.3f dev %.3f %.3f\n", r.p,
+                                     static_cast<unsigned long long>(r.words), 1e3 * r.t0, 1e3 * r.t1, 1e3 * r.t2, a, b);
+                        cudaEventDestroy(r.k0);
+                        cudaEventDestroy(r.k1);
+                    }
+                cudaEventDestroy(ev0);
             }
             for (const auto& e : errors)
                 if (!e.empty()) fail(FW2V_ERR_CUDA, e);
@@ -1070,8 +1123,9 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
         FW2V_CK(cudaSetDevice(x->cfg.device));
         const fw2v_config& cfg = x->cfg;
         const CorpusView corpus{offsets, ids, n_sentences};
-        const int P = x->producers();
-        const uint64_t chunk = (n_sentences + P - 1) / std::max(P, 1);
+        const int P = x->producers();  // streams the plan's launches are spread over
+        const int NC = x->chunks();
+        const uint64_t chunk = (n_sentences + NC - 1) / std::max(NC, 1);
         const uint64_t schedule_total =
             cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
         const Sampler sp = x->sampler();
@@ -1081,11 +1135,14 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
             std::vector<uint32_t> off;
             std::vector<float> alpha;
         };
-        std::vector<std::vector<HostBatch>> host(static_cast<size_t>(P));
+        std::vector<std::vector<HostBatch>> host(static_cast<size_t>(NC));
         std::atomic<uint64_t> reserved{x->words_trained};
         std::vector<std::thread> threads;
-        for (int p = 0; p < P; ++p) {
-            threads.emplace_back([&, p] {
+        std::atomic<int> next_chunk{0};
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        for (unsigned th = 0; th < std::min<unsigned>(hw, static_cast<unsigned>(NC)); ++th) {
+            threads.emplace_back([&] {
+              for (int p = next_chunk.fetch_add(1); p < NC; p = next_chunk.fetch_add(1)) {
                 const uint64_t begin = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
                 const uint64_t end = std::min(n_sentences, begin + chunk);
                 uint64_t cap_w, cap_s;
@@ -1108,6 +1165,7 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
                     for (uint64_t q = 0; q < kept; ++q) hb.alpha[q] = lr_at(base + bo[q], schedule_total, cfg.alpha0);
                     host[static_cast<size_t>(p)].push_back(std::move(hb));
                 }
+              }
             });
         }
         for (auto& t : threads) t.join();
@@ -1122,7 +1180,7 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
         plan->bytes = bytes;
         char* base = static_cast<char*>(plan->d_mem);
         plan->lanes.resize(static_cast<size_t>(P));
-        for (int p = 0; p < P; ++p) {
+        for (int p = 0; p < NC; ++p) {
             for (auto& hb : host[static_cast<size_t>(p)]) {
                 auto put = [&](const void* src, size_t n) {
                     char* dst = base;
@@ -1136,7 +1194,7 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
                 b.view.offsets = reinterpret_cast<const uint32_t*>(put(hb.off.data(), 4 * hb.off.size()));
                 b.view.alpha = reinterpret_cast<const float*>(put(hb.alpha.data(), 4 * hb.alpha.size()));
                 b.view.n_sentences = static_cast<int32_t>(hb.alpha.size());
-                plan->lanes[static_cast<size_t>(p)].push_back(b);
+                plan->lanes[static_cast<size_t>(p % P)].push_back(b);
                 plan->words += hb.ids.size();
                 plan->sentences += hb.alpha.size();
                 plan->batches += 1;
