@@ -70,9 +70,10 @@ typedef struct fw2v_config {
     int32_t fast_sigmoid;  /* K1 sigmoid: 1 tanh.approx (|err| < 1e-3), 0 expf */
     int32_t k1_lanes;      /* 0 = auto; else lanes per sentence (4, 8, 16, 32) */
     int32_t streams;       /* 0 = workers; batching threads, one CUDA stream each */
-    int32_t l1_refresh_log2; /* K1s Hogwild sample reads: 0 = through L2 only (exact per-sentence
-                                order); k > 0 = through L1, each SM's L1 refreshed every 2^k windows
-                                (bounded staleness for Zipf-hot rows) */
+    int32_t l1_refresh_log2; /* K1s Hogwild sample reads are staged through L1: 0 = each warp drops its
+                                SM's L1 every window (exact per-sentence order); k > 0 = one warp per
+                                block refreshes the L1 every 2^k windows (bounded staleness for
+                                Zipf-hot rows) */
     int32_t delta_writeback; /* Hogwild kernels: 1 = rows leave the ring / sweep as red.add(final -
                                 loaded) so concurrent sentences never overwrite each other's updates;
                                 0 = overwrite, the reference's per-sentence write sequence exactly */

@@ -40,9 +40,11 @@ struct ModelView {
 
 // K1s memory-path options.
 constexpr int32_t kFlagRedSamples = 1;    // sample rows: red.global.add of the delta (no lost updates)
-constexpr int32_t kFlagL1Samples = 2;     // sample prefetch through L1 (cp.async.ca)
+constexpr int32_t kFlagL1Exact = 2;       // K1s sample rows are staged through L1 (cp.async.ca); every warp
+                                          // drops its SM's L1 each window, so reads see the sentence's own writes
 constexpr int32_t kFlagDeltaRing = 4;     // ring rows written back as red.add(final - loaded)
-constexpr int32_t kFlagInvalShift = 8;    // bits 8..11: L1 invalidation every 2^k windows (0 = never)
+constexpr int32_t kFlagInvalShift = 8;    // bits 8..11: otherwise one warp per block drops the SM's L1 every
+                                          // 2^k windows (bounded staleness for Zipf-hot rows; 0 = never)
 
 // Device-side instrumented access counters, in the reference's units
 // (whole-vector accesses, traffic.hpp:19-40).

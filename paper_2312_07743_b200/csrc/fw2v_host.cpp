@@ -744,8 +744,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         // Sample rows are always written as red.global.add of the window delta
         // (row += delta, trainer.cpp:198-204); reads optionally go through L1.
         x->k1_flags = kFlagRedSamples | (cfg->delta_writeback ? kFlagDeltaRing : 0);
-        if (cfg->l1_refresh_log2 > 0)
-            x->k1_flags |= kFlagL1Samples | (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift);
+        x->k1_flags |= cfg->l1_refresh_log2 > 0 ? (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift) : kFlagL1Exact;
         if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments
         x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
                             : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives, cfg->alpha0, 0, 1) : 0;

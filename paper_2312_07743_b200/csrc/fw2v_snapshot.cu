@@ -187,17 +187,15 @@ struct Slice {
             else *reinterpret_cast<float2*>(p + c * CS) = make_float2(0.0f, 0.0f);
         }
     }
-    // Stage the lane's slice of a global row into shared memory (cp.async, L2 or L1).
-    __device__ __forceinline__ static void stage(float* dst, const float* src, bool via_l1) {
+    // Stage the lane's slice of a global row into shared memory (cp.async through L1).
+    __device__ __forceinline__ static void stage(float* dst, const float* src) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + c * CS));
-            if constexpr (CW == 4) {
-                if (via_l1) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
-                else asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
-            } else {
+            if constexpr (CW == 4)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
+            else
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + c * CS) : "memory");
-            }
         }
     }
     // row += d at L2 when pred (no branch).
@@ -344,7 +342,6 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 #pragma unroll
             SL::zero_shared(sbuf + q * STRIDE);
     }
-    const bool l1_samples = (m.flags & kFlagL1Samples) != 0;
     auto prefetch = [&](int target, const int (&nv)[MULTI ? 1 : NN], bool active, int parity) {
         float* dst = sbuf + parity * NC * STRIDE;
 #pragma unroll
@@ -352,10 +349,11 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
             const int s = q == 0 ? target : nv[q > 0 ? q - 1 : 0];
             if (active && q <= n_neg && s >= 0) {
 #pragma unroll
-                SL::stage(dst + q * STRIDE, srow(s), l1_samples);
+                SL::stage(dst + q * STRIDE, srow(s));
             }
         }
     };
+    const bool l1_exact = (m.flags & kFlagL1Exact) != 0;
     const int inval_log2 = (m.flags >> kFlagInvalShift) & 15;
     const unsigned inval_mask = inval_log2 ? (1u << inval_log2) - 1u : 0u;
     bool nraw_ok = false;
@@ -601,9 +599,13 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         }
         nraw_ok = i + 2 < L;
         tok_ahead = tok_ok ? tok_raw : -1;
-        // Bounded staleness for L1-cached sample rows: refresh this SM's L1.
-        if (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
-            (threadIdx.x >> 5) == 0) {
+        // Sample rows are staged through L1. Exact mode: this warp drops its SM's
+        // L1 before the next window's staging (fence.acq_rel.gpu -> CCTL.IVALL),
+        // so every read sees this sentence's earlier reductions. Otherwise one
+        // warp per block refreshes the L1 every 2^k windows: bounded staleness
+        // for the Zipf-hot rows, whose lines stay L1-resident in between.
+        if (l1_exact || (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
+                         (threadIdx.x >> 5) == 0)) {
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
     }

@@ -22,7 +22,7 @@
 #define KB_PAD 0
 #endif
 #ifndef KB_FLAGS
-#define KB_FLAGS (fw2v::kFlagRedSamples | fw2v::kFlagDeltaRing | fw2v::kFlagL1Samples | (5 << fw2v::kFlagInvalShift))
+#define KB_FLAGS (fw2v::kFlagRedSamples | fw2v::kFlagDeltaRing | (5 << fw2v::kFlagInvalShift))
 #endif
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
