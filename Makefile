@@ -26,7 +26,16 @@ $(BUILD)/fw2v_kernels.o: $(SRC)/fw2v_kernels.cu $(SRC)/fw2v_device.cuh
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(BUILD)/ptxas_kernels.log || (cat $(BUILD)/ptxas_kernels.log; false)
 
-$(BUILD)/fw2v_snapshot.o: $(SRC)/fw2v_snapshot.cu $(SRC)/fw2v_device.cuh $(SRC)/fw2v_common.cuh
+# K1s: one translation unit per lane shape (compiled in parallel), plus the dispatch.
+K1S_SHAPES := l4v4 l8v4 l16v4 l16v8 l32v4 l32v6 l32v8 l32v10 l32v12
+K1S_OBJS   := $(addprefix $(BUILD)/k1s_,$(addsuffix .o,$(K1S_SHAPES)))
+K1S_DEPS   := $(SRC)/fw2v_snapshot.cuh $(SRC)/fw2v_device.cuh $(SRC)/fw2v_common.cuh
+
+$(BUILD)/k1s_%.o: $(SRC)/k1s_%.cu $(K1S_DEPS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(BUILD)/ptxas_k1s_$*.log || (cat $(BUILD)/ptxas_k1s_$*.log; false)
+
+$(BUILD)/fw2v_snapshot.o: $(SRC)/fw2v_snapshot.cu $(K1S_DEPS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(BUILD)/ptxas_snapshot.log || (cat $(BUILD)/ptxas_snapshot.log; false)
 
@@ -38,7 +47,7 @@ $(BUILD)/fw2v_corpus.o: $(SRC)/fw2v_corpus.cpp include/fw2v.h
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -O3 -c -o $@ $<
 
-$(LIB)/libfw2v.so: $(BUILD)/fw2v_kernels.o $(BUILD)/fw2v_snapshot.o $(BUILD)/fw2v_host.o $(BUILD)/fw2v_corpus.o
+$(LIB)/libfw2v.so: $(BUILD)/fw2v_kernels.o $(BUILD)/fw2v_snapshot.o $(K1S_OBJS) $(BUILD)/fw2v_host.o $(BUILD)/fw2v_corpus.o
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread -ldl -lrt
 

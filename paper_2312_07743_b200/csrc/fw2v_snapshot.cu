@@ -1,718 +1,17 @@
-// K1s — FULL-W2V window kernel with independent negatives (the paper's update
-// rule; reference oracle: sweep_samples_snapshot,
-// trainer.cpp:158-205, ReuseMode::window_snapshot).
-//
-// Every (sample, context) pairing of a window is computed from window-entry
-// values, so the (N+1) x 2W_f dots of a window are independent:
-//   1. the N+1 sample rows (syn1) of window i+1 are prefetched with cp.async
-//      (16 B per lane, L2 only) into shared memory while window i computes;
-//   2. all dots are formed per lane on VEC columns with packed FFMA2
-//      (sm_100 fma.rn.f32x2) and reduced across the LANES lanes of the
-//      sentence's group with ONE transposed butterfly: at each xor level a lane
-//      keeps half of its partial sums and sends the other half, so NV dots cost
-//      ~NV shuffles in total instead of NV*log2(LANES);
-//   3. each lane evaluates the sigmoid for the dots it ended up owning and
-//      publishes g as (g, g) pairs in shared memory;
-//   4. sample deltas D_k = sum_r g_kr c_r and context updates
-//      c_r += sum_k g_kr s_k are FFMA2 on registers; samples are written once
-//      per window (row += delta, trainer.cpp:198-204).
-// The 2W_f+1 ring of syn0 rows (ContextRing, trainer.cpp:32-102) stays in
-// registers for the sentence's lifetime and slides by register renaming.
-// Positions that the reference keeps resident until finish() (the last 2W_f+1)
-// are parked in shared memory and written back in ring-slot order, so each
-// sentence's global write sequence is the reference's.
-#include <cuda_runtime.h>
-
-#include <cstdint>
-
-#include "fw2v_common.cuh"
-#include "fw2v_device.cuh"
-
-#ifdef KB_TIMING  // experiment: per-phase SM clocks of each warp, summed into kb_timing[]
-__device__ unsigned long long kb_timing[16];
-#define KB_T_DECL unsigned long long kbt[10] = {0}; long long kbt0 = clock64();
-#define KB_T(k) { const long long t_ = clock64(); kbt[k] += t_ - kbt0; kbt0 = t_; }
-#define KB_T_DUMP if (lane == 0) for (int k_ = 0; k_ < 9; ++k_) atomicAdd(&kb_timing[k_], kbt[k_]);
-#else
-#define KB_T_DECL
-#define KB_T(k)
-#define KB_T_DUMP
-#endif
+// K1s dispatch: shape (lanes x columns) -> the instantiation compiled in
+// k1s_l<L>v<V>.cu. The kernel itself is in fw2v_snapshot.cuh.
+#include "fw2v_snapshot.cuh"
 
 namespace fw2v {
 
-// Transposed butterfly over the lanes of a group (offsets O, O/2, ..., 1).
-// v[0..N) in, v[0..final) out; slot j of lane l then holds the full group sum
-// of the original index given by running plan() on an index array.
-template <int O, int N>
-struct Butterfly {
-    static constexpr int H = N / 2;
-    static constexpr int NEXT = H + (N & 1);
-    __host__ __device__ static constexpr int final_count() {
-        if constexpr (O > 1) return Butterfly<O / 2, NEXT>::final_count();
-        else return NEXT;
-    }
-
-    template <int CAP>
-    __device__ __forceinline__ static void reduce(float (&v)[CAP], int sub) {
-        static_assert(N <= CAP, "butterfly overflow");
-        const bool bit = (sub & O) != 0;
-#pragma unroll
-        for (int j = 0; j < H; ++j) {
-            const float a = v[j], b = v[j + H];
-            const float send = bit ? a : b;
-            const float keep = bit ? b : a;
-            v[j] = keep + __shfl_xor_sync(kFull, send, O);
-        }
-        if constexpr (N & 1) v[H] = v[N - 1] + __shfl_xor_sync(kFull, v[N - 1], O);
-        if constexpr (O > 1) Butterfly<O / 2, NEXT>::reduce(v, sub);
-    }
-
-    // Same result when lanes with bit O set hold v[j] and v[j + H] swapped on
-    // entry (their operands were loaded in swapped order): no selects at the top level.
-    template <int CAP>
-    __device__ __forceinline__ static void reduce_preswapped(float (&v)[CAP], int sub) {
-        static_assert(N <= CAP && (N & 1) == 0, "butterfly overflow");
-#pragma unroll
-        for (int j = 0; j < H; ++j) v[j] += __shfl_xor_sync(kFull, v[j + H], O);
-        if constexpr (O > 1) Butterfly<O / 2, NEXT>::reduce(v, sub);
-    }
-
-    template <int CAP>
-    __device__ __forceinline__ static void plan(int (&idx)[CAP], int sub) {
-        const bool bit = (sub & O) != 0;
-#pragma unroll
-        for (int j = 0; j < H; ++j) idx[j] = bit ? idx[j + H] : idx[j];
-        if constexpr (N & 1) idx[H] = idx[N - 1];
-        if constexpr (O > 1) Butterfly<O / 2, NEXT>::plan(idx, sub);
-    }
-};
-
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-constexpr int kPrefetchWindows = 16;
-
-template <int LANES, int VEC, int WF, int NC>
-struct K1sSmem {
-    static constexpr int NCTX = 2 * WF;
-    static constexpr int C = 2 * WF + 1;
-    static constexpr int NV = NC * NCTX;
-    static constexpr int GPAD = (NV + 3) & ~3;
-    static constexpr int STRIDE = LANES * VEC;
-    // Wide lane slices (VEC >= 8) hold twice the registers per lane: 64-thread
-    // blocks keep the per-block shared memory small enough for 5 blocks per SM.
-    static constexpr int THREADS = VEC >= 8 ? 64 : kK1Threads;
-    // Per group (one sentence): the window's g coefficients (scalars), the
-    // sample rows double-buffered by window parity, and the ring rows as loaded
-    // (delta write-back) or the finish() stash (overwrite) — never both.
-    static constexpr int kGroupFloats = GPAD + 2 * NC * STRIDE + C * STRIDE;
-    static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
-    static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
-    static constexpr int kRegBlocks = VEC >= 8 ? 5 : 3;
-    static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
-};
-
-// A lane's slice of a row: VEC = 2*H2 columns as chunks of CW floats (16 bytes
-// when H2 is even, else 8 bytes, e.g. d=300 on 32 lanes x 10 columns) spaced
-// CS = CW*LANES floats apart (chunk c of lane l at column CW*(c*LANES + l)), so
-// one chunk access by a lane group covers a contiguous CW*4*LANES-byte span:
-// coalesced in HBM/L2 and bank-conflict free in shared memory.
-template <int H2, int LANES>
-struct Slice {
-    static constexpr int CW = H2 % 2 == 0 ? 4 : 2;
-    static constexpr int CS = CW * LANES;
-    static constexpr int NCH = 2 * H2 / CW;
-    __device__ __forceinline__ static const float* chunk(const float* p, int c) { return p + c * CS; }
-    __device__ __forceinline__ static void load(float2 (&v)[H2], const float* p) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if constexpr (CW == 4) {
-                const float4 t = __ldcg(reinterpret_cast<const float4*>(p + c * CS));
-                v[2 * c] = make_float2(t.x, t.y);
-                v[2 * c + 1] = make_float2(t.z, t.w);
-            } else {
-                v[c] = __ldcg(reinterpret_cast<const float2*>(p + c * CS));
-            }
-        }
-    }
-    __device__ __forceinline__ static void load_early(float2 (&v)[H2], const float* p) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if constexpr (CW == 4) {
-                const float4 t = ldcg_early(p + c * CS);
-                v[2 * c] = make_float2(t.x, t.y);
-                v[2 * c + 1] = make_float2(t.z, t.w);
-            } else {
-                asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v[c].x), "=f"(v[c].y) : "l"(p + c * CS));
-            }
-        }
-    }
-    __device__ __forceinline__ static void store(float* p, const float2 (&v)[H2]) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if constexpr (CW == 4)
-                __stcg(reinterpret_cast<float4*>(p + c * CS), make_float4(v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y));
-            else
-                __stcg(reinterpret_cast<float2*>(p + c * CS), v[c]);
-        }
-    }
-    __device__ __forceinline__ static void load_shared(float2 (&v)[H2], const float* p) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if constexpr (CW == 4) {
-                const float4 t = *reinterpret_cast<const float4*>(p + c * CS);
-                v[2 * c] = make_float2(t.x, t.y);
-                v[2 * c + 1] = make_float2(t.z, t.w);
-            } else {
-                v[c] = *reinterpret_cast<const float2*>(p + c * CS);
-            }
-        }
-    }
-    __device__ __forceinline__ static void store_shared(float* p, const float2 (&v)[H2]) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if constexpr (CW == 4)
-                *reinterpret_cast<float4*>(p + c * CS) = make_float4(v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
-            else
-                *reinterpret_cast<float2*>(p + c * CS) = v[c];
-        }
-    }
-    __device__ __forceinline__ static void zero_shared(float* p) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if constexpr (CW == 4) *reinterpret_cast<float4*>(p + c * CS) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-            else *reinterpret_cast<float2*>(p + c * CS) = make_float2(0.0f, 0.0f);
-        }
-    }
-    // Stage the lane's slice of a global row into shared memory (cp.async through L1).
-    __device__ __forceinline__ static void stage(float* dst, const float* src) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + c * CS));
-            if constexpr (CW == 4)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
-            else
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + c * CS) : "memory");
-        }
-    }
-    // row += d at L2 when pred (no branch).
-    __device__ __forceinline__ static void red_add_if(bool pred, float* p, const float2 (&d)[H2]) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if constexpr (CW == 4) {
-                asm volatile(
-                    "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-                    "@q red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p + c * CS),
-                    "f"(d[2 * c].x), "f"(d[2 * c].y), "f"(d[2 * c + 1].x), "f"(d[2 * c + 1].y), "r"(static_cast<int>(pred))
-                    : "memory");
-            } else {
-                asm volatile(
-                    "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
-                    "@q red.global.add.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p + c * CS),
-                    "f"(d[c].x), "f"(d[c].y), "r"(static_cast<int>(pred))
-                    : "memory");
-            }
-        }
-    }
-    // row += (v - entry): the ring row's accumulated update since it was loaded.
-    __device__ __forceinline__ static void red_delta(float* p, const float2 (&v)[H2], const float* entry_smem) {
-        float2 e[H2];
-        load_shared(e, entry_smem);
-#pragma unroll
-        for (int i = 0; i < H2; ++i) e[i] = make_float2(v[i].x - e[i].x, v[i].y - e[i].y);
-        red_add_if(true, p, e);
-    }
-};
-
-template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
-__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC>::THREADS, K1sSmem<LANES, VEC, WF, NC>::MINB)
-k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) {
-    static_assert(VEC % 2 == 0, "K1s stages 8- or 16-byte chunks");
-    using SM = K1sSmem<LANES, VEC, WF, NC>;
-    constexpr int NCTX = SM::NCTX;
-    constexpr int C = SM::C;
-    constexpr int NV = SM::NV;
-    constexpr int H2 = VEC / 2;
-    constexpr int STRIDE = SM::STRIDE;
-    constexpr int HALF = LANES / 2;
-    constexpr int NN = NC - 1;  // negatives per window held by every lane (single-chunk path)
-    // Stale-prefetch detection by one __match_any_sync: lanes q < NC of a group
-    // carry this window's sample ids, lanes HALF + q the previous window's.
-    constexpr bool kMatch = NC <= HALF;
-    // The top butterfly level pairs samples q and q + NC/2 of one context row;
-    // lanes of the upper half load those two sample rows in swapped order, so
-    // that level needs no selects.
-    constexpr bool kPreswap = NC % 2 == 0;
-    using SL = Slice<H2, LANES>;
-    using BF = Butterfly<LANES / 2, NV>;
-    constexpr int NF = BF::final_count();
-    static_assert(NV <= 255 && NC <= 16 && NCTX <= 16, "slot words");
-    extern __shared__ __align__(16) float k1s_sh[];
-
-    const int lane = threadIdx.x & 31;
-    const int sub = lane & (LANES - 1);
-    const int grp = lane / LANES;
-    const int sent = static_cast<int>((blockIdx.x * SM::THREADS + threadIdx.x) / LANES);
-    const bool has = sent < b.n_sentences;
-    float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
-    float* sbuf = gsh + SM::GPAD + sub * SL::CW;                  // + (parity*NC + q)*STRIDE
-    float* ring = gsh + SM::GPAD + 2 * NC * STRIDE + sub * SL::CW;  // + slot*STRIDE
-    const bool delta_wb = (m.flags & kFlagDeltaRing) != 0;
-
-    uint32_t beg = 0, len = 0;
-    float alpha = 0.0f;
-    if (has) {
-        beg = __ldg(b.offsets + sent);
-        len = __ldg(b.offsets + sent + 1) - beg;
-        alpha = __ldg(b.alpha + sent);
-    }
-    const int L = static_cast<int>(len);
-    const int Lmax = static_cast<int>(__reduce_max_sync(kFull, len));
-    if (Lmax == 0) return;
-
-    const int32_t* __restrict__ ids = b.ids + beg;
-    const int32_t* __restrict__ negs = b.negs + static_cast<size_t>(beg) * n_neg;
-    // Row offsets use the compile-time stride (host checks |V| * stride < 2^31).
-    float* __restrict__ syn0 = m.syn0 + sub * SL::CW;
-    float* __restrict__ syn1 = m.syn1 + sub * SL::CW;
-    // Output row of sample s >= 0: hot rows go to this sentence's replica.
-    float* const hot_base = m.hot_k > 0 ? m.hot + (sent % m.hot_r) * m.hot_k * STRIDE + sub * SL::CW : syn1;
-    const int hot_k = m.hot_k;
-    auto srow = [&](int s) { return (s < hot_k ? hot_base : syn1) + s * STRIDE; };
-    const int tail = L - C;  // positions >= tail stay resident until finish()
-
-    // After the butterfly, slot j of this lane holds dot idx = q*NCTX + r. One
-    // opaque word per slot (the compiler would otherwise re-derive the plan
-    // every window): g index | r << 8 | q << 12 | (q <= N) << 16 | (q == 0) << 17.
-    unsigned slotw[NF];
-    {
-        int idx[NV];
-#pragma unroll
-        for (int j = 0; j < NV; ++j) idx[j] = j;
-        BF::plan(idx, sub);
-#pragma unroll
-        for (int j = 0; j < NF; ++j) {
-            const int q = idx[j] / NCTX, r = idx[j] - q * NCTX;
-            slotw[j] = static_cast<unsigned>(idx[j]) | (static_cast<unsigned>(r) << 8) |
-                       (static_cast<unsigned>(q) << 12) | ((q <= n_neg ? 1u : 0u) << 16) | ((q == 0 ? 1u : 0u) << 17);
-            asm volatile("" : "+r"(slotw[j]));
-        }
-    }
-    const int swap_off = (kPreswap && (sub & HALF) != 0) ? (NC / 2) * STRIDE : 0;
-
-    float2 ctx[NCTX][H2];
-    int tok[NCTX];
-    float2 tgt[H2];
-    int ttok = L > 0 ? __ldg(ids) : -1;
-    if (ttok >= 0) SL::load(tgt, syn0 + ttok * STRIDE); else vzero2(tgt);
-    if (delta_wb) SL::store_shared(ring, tgt);  // position 0 -> slot 0
-#pragma unroll
-    for (int r = 0; r < NCTX; ++r) {
-        const int p = r - WF + 1;
-        tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
-        if (tok[r] >= 0) SL::load(ctx[r], syn0 + tok[r] * STRIDE); else vzero2(ctx[r]);
-        if (delta_wb && r >= WF) SL::store_shared(ring + p * STRIDE, ctx[r]);  // p < C
-    }
-    unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
-    unsigned s_rw = 0, pairs = 0;
-
-    // Single-chunk path: every lane holds the negatives of windows i (ncur),
-    // i+1 (nnext, for the prefetch) and, raw, i+2 (loaded one window early).
-    int ncur[MULTI ? 1 : NN], nnext[MULTI ? 1 : NN], nraw[MULTI ? 1 : NN];
-    if constexpr (!MULTI) {
-#pragma unroll
-        for (int k = 0; k < NN; ++k) {
-            ncur[k] = (k < n_neg && L >= 2) ? __ldg(negs + k) : -1;
-            nnext[k] = (k < n_neg && 1 < L) ? __ldg(negs + n_neg + k) : -1;
-            nraw[k] = -1;
-        }
-    }
-    int tok_ahead = WF + 1 < L ? __ldg(ids + WF + 1) : -1;  // incoming position of window 0
-    int prev_v = -1 - lane;  // match lanes: previous window's sample id
-    int psid[kMatch ? 1 : NC];
-#pragma unroll
-    for (int q = 0; q < (kMatch ? 1 : NC); ++q) psid[q] = -100;
-
-    {
-#pragma unroll
-        for (int q = 0; q < 2 * NC; ++q)
-#pragma unroll
-            SL::zero_shared(sbuf + q * STRIDE);
-    }
-    auto prefetch = [&](int target, const int (&nv)[MULTI ? 1 : NN], bool active, int parity) {
-        float* dst = sbuf + parity * NC * STRIDE;
-#pragma unroll
-        for (int q = 0; q < NC; ++q) {
-            const int s = q == 0 ? target : nv[q > 0 ? q - 1 : 0];
-            if (active && q <= n_neg && s >= 0) {
-#pragma unroll
-                SL::stage(dst + q * STRIDE, srow(s));
-            }
-        }
-    };
-    const bool l1_exact = (m.flags & kFlagL1Exact) != 0;
-    const int inval_log2 = (m.flags >> kFlagInvalShift) & 15;
-    const unsigned inval_mask = inval_log2 ? (1u << inval_log2) - 1u : 0u;
-    bool nraw_ok = false;
-    if constexpr (!MULTI) {
-        prefetch(ttok, ncur, L >= 2, 0);  // window 0's samples
-        cp_async_commit();
-    }
-    float2 dctx[MULTI ? NCTX : 1][H2];
-
-    KB_T_DECL
-    for (int i = 0; i < Lmax; ++i) {
-        const bool act = i < L;
-        const bool wact = act && L >= 2;
-        unsigned vmask = 0;
-#pragma unroll
-        for (int r = 0; r < NCTX; ++r) vmask |= (tok[r] >= 0 ? 1u : 0u) << r;
-        const int q_in = i + 1 + WF;
-        // Token ids run one window ahead of their rows and negatives two; loads
-        // issued early are carried raw and masked where consumed. The
-        // id/negative streams are pulled into L2 kPrefetchWindows ahead.
-        if constexpr (!MULTI) {
-            if (i > 0) {
-#pragma unroll
-                for (int k = 0; k < NN; ++k) nnext[k] = (nraw_ok && k < n_neg) ? nraw[k] : -1;
-            }
-        }
-        // Next window's sample rows first (their buffer was last read in window
-        // i-1); one cp.async group per window, so the wait below can leave it in flight.
-        unsigned stale = 0;
-        if constexpr (!MULTI) {
-            if (i + 1 < Lmax) prefetch(tok[WF], nnext, i + 1 < L && L >= 2, (i + 1) & 1);
-            cp_async_commit();
-            // This window's rows the previous window rewrote after their prefetch
-            // was issued (computed here, off the critical path).
-            if constexpr (kMatch) {
-                const int q = sub & (HALF - 1);
-                int cv = ttok;
-#pragma unroll
-                for (int k = 0; k < NN; ++k) cv = q == k + 1 ? ncur[k] : cv;
-                cv = (wact && q <= n_neg && q < NC) ? cv : -1 - lane;
-                const int mv = sub < HALF ? cv : prev_v;
-                const unsigned mm = __match_any_sync(kFull, mv);
-                const unsigned upper = ((1u << HALF) - 1u) << (grp * LANES + HALF);
-                const bool st = sub < HALF && (mm & upper) != 0u;
-                stale = (__ballot_sync(kFull, st) >> (grp * LANES)) & ((1u << NC) - 1u);
-                prev_v = cv;
-            } else {
-                int sq[NC];
-#pragma unroll
-                for (int q = 0; q < NC; ++q) sq[q] = (wact && q <= n_neg) ? (q == 0 ? ttok : ncur[q > 0 ? q - 1 : 0]) : -1 - q;
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    bool st = false;
-#pragma unroll
-                    for (int j = 0; j < NC; ++j) st |= sq[q] == psid[j];
-                    stale |= (st ? 1u : 0u) << q;
-                }
-#pragma unroll
-                for (int q = 0; q < NC; ++q) psid[q] = sq[q] >= 0 ? sq[q] : -100;
-            }
-        }
-        const int inc_tok = tok_ahead;
-        float2 inc[H2];
-        SL::load_early(inc, syn0 + max(inc_tok, 0) * STRIDE);
-        const int last = max(L - 1, 0);
-        const int tok_raw = ldg_early(ids + min(q_in + 1, last));
-        if constexpr (!MULTI) {
-            const int* nrow = negs + static_cast<size_t>(min(i + 2, last)) * n_neg;
-#pragma unroll
-            for (int k = 0; k < NN; ++k) nraw[k] = n_neg > 0 ? ldg_early(nrow + min(k, n_neg - 1)) : -1;
-        }
-        const bool tok_ok = q_in + 1 < L;
-        if (sub == 0 && i + kPrefetchWindows < L) {
-            prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * n_neg);
-            prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
-        }
-        c_reads += inc_tok >= 0;
-        if constexpr (MULTI) {
-#pragma unroll
-            for (int r = 0; r < NCTX; ++r) vzero2(dctx[r]);
-        }
-
-        const int n_chunks = MULTI ? (n_neg + NC) / NC : 1;
-        for (int ch = 0; ch < n_chunks; ++ch) {
-            const int kbase = MULTI ? ch * NC : 0;
-            int sid[NC];
-#pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                const int kk = kbase + q;
-                int s;
-                if constexpr (MULTI) s = (kk == 0) ? ttok : (wact && kk <= n_neg ? __ldg(negs + i * n_neg + kk - 1) : -1);
-                else s = q == 0 ? ttok : ncur[q > 0 ? q - 1 : 0];
-                sid[q] = (wact && kk <= n_neg) ? s : -1 - q;  // empty slots: distinct negative ids
-            }
-            const float* cur = sbuf;
-            if constexpr (!MULTI) {
-                // Rows staged by cp.async during the previous window; slots
-                // without a sample hold finite stale rows and get g = 0.
-                KB_T(0)
-                cp_async_wait_group<1>();
-                KB_T(1)
-                cur = sbuf + (i & 1) * NC * STRIDE;
-                if (stale != 0u) {
-#pragma unroll
-                    for (int q = 0; q < NC; ++q)
-                        if (((stale >> q) & 1u) && sid[q] >= 0) {
-                            float2 v[H2];
-                            SL::load(v, srow(sid[q]));
-                            SL::store_shared(const_cast<float*>(cur) + q * STRIDE, v);
-                        }
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    float2 v[H2];
-                    SL::load(v, srow(max(sid[q], 0)));
-                    SL::store_shared(sbuf + q * STRIDE, v);
-                }
-            }
-
-            KB_T(2)
-            // 1-2. all dots of the chunk (window-entry values), one transposed butterfly.
-            float P[NV];
-            {
-                const float* lo = cur + swap_off;  // samples q < NC/2 (or their partners)
-                const float* hi = cur - swap_off;
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    float2 S[H2];
-                    SL::load_shared(S, (kPreswap && q < NC / 2 ? lo : (kPreswap ? hi : cur)) + q * STRIDE);
-#pragma unroll
-                    for (int r = 0; r < NCTX; ++r) {
-                        float2 acc = __fmul2_rn(ctx[r][0], S[0]);
-#pragma unroll
-                        for (int h = 1; h < H2; ++h) acc = __ffma2_rn(ctx[r][h], S[h], acc);
-                        P[q * NCTX + r] = acc.x + acc.y;
-                    }
-                }
-            }
-            KB_T(3)
-            if constexpr (kPreswap) BF::reduce_preswapped(P, sub);
-            else BF::reduce(P, sub);
-
-            KB_T(4)
-            // 3. sigmoid on the owned dots; g published as scalars [q][r].
-#pragma unroll
-            for (int j = 0; j < NF; ++j) {
-                const unsigned w = slotw[j];
-                const bool vbit = ((vmask >> ((w >> 8) & 15u)) & 1u) != 0u;
-                bool valid;
-                float label;
-                if constexpr (MULTI) {
-                    const int kk = kbase + static_cast<int>((w >> 12) & 15u);
-                    valid = wact && kk <= n_neg && vbit;
-                    label = kk == 0 ? 1.0f : 0.0f;
-                } else {
-                    valid = wact && ((w >> 16) & 1u) && vbit;
-                    label = ((w >> 17) & 1u) ? 1.0f : 0.0f;
-                }
-                gsh[w & 255u] = valid ? sgd_coeff<FAST>(P[j], label, alpha) : 0.0f;
-            }
-            __syncwarp();
-            float g[SM::GPAD];
-#pragma unroll
-            for (int k = 0; k < SM::GPAD; k += 4) {
-                const float4 t = *reinterpret_cast<const float4*>(gsh + k);
-                g[k] = t.x; g[k + 1] = t.y; g[k + 2] = t.z; g[k + 3] = t.w;
-            }
-            __syncwarp();
-
-            KB_T(5)
-            // 4a. sample deltas from window-entry context rows, written back as
-            //     row += delta at L2 (trainer.cpp:198-204, duplicates included).
-#pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                float2 D[H2];
-#pragma unroll
-                for (int h = 0; h < H2; ++h) D[h] = __fmul2_rn(make_float2(g[q * NCTX], g[q * NCTX]), ctx[0][h]);
-#pragma unroll
-                for (int r = 1; r < NCTX; ++r)
-#pragma unroll
-                    for (int h = 0; h < H2; ++h)
-                        D[h] = __ffma2_rn(make_float2(g[q * NCTX + r], g[q * NCTX + r]), ctx[r][h], D[h]);
-                SL::red_add_if(sid[q] >= 0, srow(max(sid[q], 0)), D);
-            }
-            KB_T(6)
-            // 4b. context rows from window-entry sample rows.
-#pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                float2 S[H2];
-                SL::load_shared(S, cur + q * STRIDE);
-#pragma unroll
-                for (int r = 0; r < NCTX; ++r) {
-                    const float2 gg = make_float2(g[q * NCTX + r], g[q * NCTX + r]);
-#pragma unroll
-                    for (int h = 0; h < H2; ++h) {
-                        if constexpr (MULTI) dctx[r][h] = __ffma2_rn(gg, S[h], dctx[r][h]);
-                        else ctx[r][h] = __ffma2_rn(gg, S[h], ctx[r][h]);
-                    }
-                }
-            }
-            if constexpr (MULTI) __syncwarp();  // the next chunk rewrites sbuf
-        }
-        if constexpr (MULTI) {
-#pragma unroll
-            for (int r = 0; r < NCTX; ++r)
-#pragma unroll
-                for (int h = 0; h < H2; ++h) ctx[r][h] = __fadd2_rn(ctx[r][h], dctx[r][h]);
-        }
-        if (wact) {
-            s_rw += static_cast<unsigned>(n_neg + 1);
-            pairs += static_cast<unsigned>(__popc(vmask)) * static_cast<unsigned>(n_neg + 1);
-        }
-
-        KB_T(7)
-        // Slide the ring (ContextRing::advance, trainer.cpp:55-69).
-        const int etok = tok[0];
-        if (etok >= 0) {
-            const int p = i - WF;
-            if (delta_wb) {
-                SL::red_delta(syn0 + etok * STRIDE, ctx[0], ring + (p % C) * STRIDE);
-            } else if (p >= tail) {
-                SL::store_shared(ring + (p % C) * STRIDE, ctx[0]);
-            } else {
-                SL::store(syn0 + etok * STRIDE, ctx[0]);
-            }
-            if (inc_tok == etok) vcopy2(inc, ctx[0]);
-        }
-        if (delta_wb && inc_tok >= 0) SL::store_shared(ring + (q_in % C) * STRIDE, inc);
-#pragma unroll
-        for (int r = 0; r < WF - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
-        vcopy2(ctx[WF - 1], tgt);
-        tok[WF - 1] = act ? ttok : -1;
-        vcopy2(tgt, ctx[WF]);
-        ttok = tok[WF];
-#pragma unroll
-        for (int r = WF; r < NCTX - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
-        vcopy2(ctx[NCTX - 1], inc);
-        tok[NCTX - 1] = inc_tok;
-        if constexpr (!MULTI) {
-#pragma unroll
-            for (int k = 0; k < NN; ++k) ncur[k] = nnext[k];
-        }
-        nraw_ok = i + 2 < L;
-        tok_ahead = tok_ok ? tok_raw : -1;
-        // Sample rows are staged through L1. Exact mode: this warp drops its SM's
-        // L1 before the next window's staging (fence.acq_rel.gpu -> CCTL.IVALL),
-        // so every read sees this sentence's earlier reductions. Otherwise one
-        // warp per block refreshes the L1 every 2^k windows: bounded staleness
-        // for the Zipf-hot rows, whose lines stay L1-resident in between.
-        if (l1_exact || (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
-                         (threadIdx.x >> 5) == 0)) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        }
-    }
-    KB_T(8)
-    KB_T_DUMP
-    // ContextRing::finish (trainer.cpp:71-75): residents in slot order.
-    const int i_end = Lmax;  // registers hold positions i_end-WF .. i_end+WF
-    if (delta_wb) {
-        // Deltas commute: no ordering to preserve.
-#pragma unroll
-        for (int r = 0; r < NCTX; ++r) {
-            const int p = r < WF ? i_end - WF + r : i_end + 1 + (r - WF);
-            if (tok[r] >= 0) SL::red_delta(syn0 + tok[r] * STRIDE, ctx[r], ring + (p % C) * STRIDE);
-        }
-        if (ttok >= 0) SL::red_delta(syn0 + ttok * STRIDE, tgt, ring + (i_end % C) * STRIDE);
-    } else {
-#pragma unroll
-        for (int r = 0; r < NCTX; ++r) {
-            const int p = r < WF ? i_end - WF + r : i_end + 1 + (r - WF);
-            if (tok[r] >= 0) SL::store_shared(ring + (p % C) * STRIDE, ctx[r]);
-        }
-        if (ttok >= 0) SL::store_shared(ring + (i_end % C) * STRIDE, tgt);
-        const int first = max(0, tail);
-        for (int s = 0; s < C; ++s) {
-            // the resident position in slot s: first + ((s - first) mod C), if < L
-            const int p = first + ((s - first % C) + C) % C;
-            if (p < L) {
-                float2 v[H2];
-                SL::load_shared(v, ring + s * STRIDE);
-                SL::store(syn0 + __ldg(ids + p) * STRIDE, v);
-            }
-        }
-    }
-
-    if (ctr != nullptr) {
-        const bool lead = has && sub == 0;
-        const unsigned hits = (L >= 2) ? pairs - static_cast<unsigned>(L) : 0u;
-        const unsigned v0 = __reduce_add_sync(kFull, lead ? c_reads : 0u);
-        const unsigned v2 = __reduce_add_sync(kFull, lead ? s_rw : 0u);
-        const unsigned v4 = __reduce_add_sync(kFull, lead ? hits : 0u);
-        const unsigned v5 = __reduce_add_sync(kFull, lead ? static_cast<unsigned>(L) : 0u);
-        const unsigned v6 = __reduce_add_sync(kFull, lead ? 1u : 0u);
-        if (lane == 0) {
-            atomicAdd(&ctr->context_reads, v0);
-            atomicAdd(&ctr->context_writes, v5);  // every position is written back exactly once
-            atomicAdd(&ctr->sample_reads, v2);
-            atomicAdd(&ctr->sample_writes, v2);
-            atomicAdd(&ctr->ring_hits, v4);
-            atomicAdd(&ctr->words, v5);
-            atomicAdd(&ctr->sentences, v6);
-        }
-    }
-}
-
-// ------------------------------------------------------------------ dispatch
-template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
-cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, int n_neg, DevCounters* ctr,
-                            cudaStream_t st, int* resident) {
-    constexpr int bytes = K1sSmem<LANES, VEC, WF, NC>::kBlockBytes;
-    auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MULTI, FAST>;
-    static bool configured = false;  // benign race: idempotent attribute set
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    constexpr int threads = K1sSmem<LANES, VEC, WF, NC>::THREADS;
-    if (resident != nullptr) return resident_sentences(kern, bytes, threads, threads / LANES, resident);
-    if (blocks == 0) return cudaSuccess;
-    kern<<<blocks, K1sSmem<LANES, VEC, WF, NC>::THREADS, bytes, st>>>(m, b, n_neg, ctr);
-    return cudaGetLastError();
-}
-
-template <int LANES, int VEC, int WF, int NC>
-cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
-                          cudaStream_t st, int* resident) {
-    constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;
-    const int blocks = (b.n_sentences + per_block - 1) / per_block;
-    const bool multi = n_neg + 1 > NC;
-    if (multi) {
-        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, true, true>(blocks, m, b, n_neg, ctr, st, resident)
-                    : launch_k1s_inst<LANES, VEC, WF, NC, true, false>(blocks, m, b, n_neg, ctr, st, resident);
-    }
-    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, false, true>(blocks, m, b, n_neg, ctr, st, resident)
-                : launch_k1s_inst<LANES, VEC, WF, NC, false, false>(blocks, m, b, n_neg, ctr, st, resident);
-}
-
-template <int LANES, int VEC>
-cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
-                             DevCounters* ctr, cudaStream_t st, int* resident) {
-    switch (wf) {
-    case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, ctr, st, resident);
-    case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, ctr, st, resident);
-    case 3: return launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, ctr, st, resident);
-    // Wide windows: one 6-sample chunk when N+1 <= 6, else 4-sample chunks (registers).
-    case 4: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 4, 6>(m, b, n_neg, fast, ctr, st, resident)
-                                  : launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, ctr, st, resident);
-    case 5: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 5, 6>(m, b, n_neg, fast, ctr, st, resident)
-                                  : launch_k1s_nc<LANES, VEC, 5, 4>(m, b, n_neg, fast, ctr, st, resident);
-    default: return cudaErrorInvalidValue;
-    }
-}
-
 #define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(16, 8) X(32, 4) X(32, 6) X(32, 8) X(32, 10) X(32, 12)
 
-// Requires n_neg <= 2 * LANES (negatives are distributed two per lane).
-#ifndef FW2V_KBENCH  // tools/kbench.cu instantiates single kernels directly
+#define FW2V_EXTERN(L_, V_)                                                                                 \
+    extern template cudaError_t launch_k1s_shape<L_, V_>(const ModelView&, const BatchView&, int, int, bool, \
+                                                         DevCounters*, cudaStream_t, int*);
+FW2V_K1S_SHAPES(FW2V_EXTERN)
+#undef FW2V_EXTERN
+
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
                        DevCounters* ctr, cudaStream_t st, int* resident) {
 #define FW2V_CASE(L_, V_) \
@@ -722,14 +21,14 @@ cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& 
     return cudaErrorInvalidValue;
 }
 
+// Any N: N + 1 <= 6 samples run as one chunk with the negatives in registers,
+// more as chunks of 4 or 6 loaded per window.
 bool k1s_supported(int lanes, int vec, int n_neg, int wf) {
-    if (n_neg > 2 * lanes || wf < 1 || wf > 5) return false;
+    if (n_neg < 0 || wf < 1 || wf > 5) return false;
 #define FW2V_CASE(L_, V_) if (lanes == L_ && vec == V_) return true;
     FW2V_K1S_SHAPES(FW2V_CASE)
 #undef FW2V_CASE
     return false;
 }
-
-#endif
 
 } // namespace fw2v

@@ -1,0 +1,8 @@
+// K1s instantiation for 16 lanes x 8 columns (one translation unit per shape
+// so the sm_100a build compiles them in parallel).
+#include "fw2v_snapshot.cuh"
+
+namespace fw2v {
+template cudaError_t launch_k1s_shape<16, 8>(const ModelView&, const BatchView&, int, int, bool, DevCounters*,
+                                               cudaStream_t, int*);
+} // namespace fw2v

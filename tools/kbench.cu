@@ -1,8 +1,7 @@
 // K1s microbenchmark: one kernel instantiation on the text8-shaped epoch as a
 // single device-resident batch (exact reference batcher from libfw2v.so).
 // Build variants with -D flags (see tools/kbench.sh); prints words/s.
-#define FW2V_KBENCH 1
-#include "../paper_2312_07743_b200/csrc/fw2v_snapshot.cu"
+#include "../paper_2312_07743_b200/csrc/fw2v_snapshot.cuh"
 
 #include <cmath>
 #include <cstdio>
