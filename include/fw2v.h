@@ -205,6 +205,18 @@ float fw2v_lr_at(uint64_t words_trained, uint64_t total, float alpha0);
 int fw2v_analytic_traffic(uint64_t length, int32_t width, int32_t negatives, int32_t mode,
                           fw2v_counters* out);
 
+/* Embedding text writer: save_embeddings (model.cpp:47-74)
+ * byte for byte — "<|V|> <dim>\n", then per row the token and " <value>" per
+ * column with std::to_chars fixed, 6 decimals — formatted on `threads` host
+ * threads (<= 0: all cores). rows: |V| x dim host floats, row stride
+ * row_stride >= dim; tokens: concatenated token bytes, token_offsets[|V|+1].
+ * FW2V_ERR_IO on open/write failure (ringvec ErrorCode::io). */
+int fw2v_write_embeddings(const float* rows, int32_t vocab_size, int32_t dim, int64_t row_stride,
+                          const char* tokens, const uint64_t* token_offsets, const char* path, int32_t threads);
+/* The same straight from a trainer's device model: which = 0 input (syn0), 1 output (syn1). */
+int fw2v_save_model(fw2v_ctx* ctx, int32_t which, const char* tokens, const uint64_t* token_offsets,
+                    const char* path, int32_t threads);
+
 /* Synthetic Zipf corpus of the benchmark shapes (bench
  * input, not the training path): `tokens` i.i.d. ranks r in 1..types with
  * p(r) ∝ r^-s (inverse CDF by binary search; token i uses splitmix64 draw i of

@@ -136,6 +136,14 @@ class Oracle:
         if rc != 0:
             raise RuntimeError(f"{self.kind}: error {rc}: {self._fn('last_error')().decode()}")
 
+    def save_embeddings(self, path, rows, counts, which=0):
+        """Reference save_embeddings with the ref_capi token names (w%09d); ref only."""
+        rows = np.ascontiguousarray(rows, np.float32)
+        counts = np.ascontiguousarray(counts, np.uint64)
+        self._check(self._fn("save_embeddings")(counts.ctypes.data_as(C.POINTER(C.c_uint64)), rows.shape[0],
+                                                rows.shape[1], rows.ctypes.data_as(C.POINTER(C.c_float)), which,
+                                                os.fsencode(str(path))))
+
     # -- scalar helpers ------------------------------------------------------
     def sigmoid(self, x: float) -> float:
         return self._fn("sigmoid")(x)

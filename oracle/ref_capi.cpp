@@ -16,6 +16,7 @@
 //   ref_assemble_batch   -> ringvec::assemble_batch        sampler.cpp:41
 //   ref_rng_draws        -> ringvec::Rng::derive/next_u64  rng.hpp:16-28
 //   ref_analytic_traffic -> ringvec::analytic_traffic      traffic.cpp:21
+//   ref_save_embeddings  -> ringvec::save_embeddings       model.cpp:47-74
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -312,6 +313,25 @@ int ref_analytic_traffic(uint64_t length, int32_t width, int32_t negatives, int3
                          uint64_t* out) {
     try {
         fill_counters(out, analytic_traffic(length, width, negatives, static_cast<ReuseMode>(mode)));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// save_embeddings of a |V| x dim matrix with the ref_capi token names
+// (w%09d) and the given counts (non-increasing); which: 0 input, 1 output.
+int ref_save_embeddings(const uint64_t* counts, int32_t vocab_size, int32_t dim, const float* rows,
+                        int32_t which, const char* path) {
+    try {
+        Vocabulary v = vocab_from_counts(counts, vocab_size);
+        EmbeddingModel m;
+        m.vocab_size = vocab_size;
+        m.dim = dim;
+        const size_t n = static_cast<size_t>(vocab_size) * static_cast<size_t>(dim);
+        m.input.assign(rows, rows + n);
+        m.output.assign(rows, rows + n);
+        save_embeddings(m, v, path, which == 0 ? MatrixKind::input : MatrixKind::output);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

@@ -47,6 +47,8 @@ cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st);
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
                        DevCounters* ctr, cudaStream_t st, int* resident = nullptr);
 bool k1s_supported(int lanes, int vec, int n_neg, int wf);
+int write_embeddings(const float* rows, int32_t vocab_size, int32_t dim, int64_t row_stride, const char* tokens,
+                     const uint64_t* token_offsets, const char* path, int32_t threads, std::string* err);
 } // namespace fw2v
 
 namespace {
@@ -825,6 +827,28 @@ int fw2v_set_model(fw2v_ctx* x, const float* input, const float* output) {
             FW2V_CK(cudaMemcpy2D(x->syn1, p, output, w, w, static_cast<size_t>(x->vocab), cudaMemcpyHostToDevice));
         }
     });
+}
+
+int fw2v_save_model(fw2v_ctx* x, int32_t which, const char* tokens, const uint64_t* token_offsets, const char* path,
+                    int32_t threads) {
+    std::vector<float> host;
+    int rc = guarded([&] {
+        if (which != 0 && which != 1) fail(FW2V_ERR_BAD_ARGUMENT, "which must be 0 (input) or 1 (output)");
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        host.resize(static_cast<size_t>(x->vocab) * static_cast<size_t>(x->stride));
+        FW2V_CK(cudaMemcpy(host.data(), which == 0 ? x->syn0 : x->syn1, sizeof(float) * host.size(),
+                           cudaMemcpyDeviceToHost));
+    });
+    if (rc != FW2V_OK) return rc;
+    return fw2v_write_embeddings(host.data(), x->vocab, x->cfg.dim, x->stride, tokens, token_offsets, path, threads);
+}
+
+int fw2v_write_embeddings(const float* rows, int32_t vocab_size, int32_t dim, int64_t row_stride, const char* tokens,
+                          const uint64_t* token_offsets, const char* path, int32_t threads) {
+    std::string err;
+    const int rc = write_embeddings(rows, vocab_size, dim, row_stride, tokens, token_offsets, path, threads, &err);
+    if (rc != FW2V_OK) g_error = err;
+    return rc;
 }
 
 int fw2v_model_device(fw2v_ctx* x, float** syn0, float** syn1, int32_t* stride) {

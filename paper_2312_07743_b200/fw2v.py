@@ -251,6 +251,24 @@ def analytic_traffic(length, width, negatives, mode="lifetime"):
 
 
 # ------------------------------------------------------------ synthetic corpora
+def _token_blob(tokens):
+    enc = [t.encode() if isinstance(t, str) else bytes(t) for t in tokens]
+    offs = np.zeros(len(enc) + 1, np.uint64)
+    offs[1:] = np.cumsum([len(e) for e in enc])
+    blob = C.create_string_buffer(b"".join(enc), int(offs[-1]) + 1)
+    return blob, offs
+
+
+def write_embeddings(path, rows, tokens, threads=0):
+    """save_embeddings (model.cpp:47-74) byte for byte, on all host cores."""
+    rows = np.ascontiguousarray(rows, np.float32)
+    if rows.ndim != 2 or rows.shape[0] != len(tokens):
+        raise ValueError("rows must be |V| x dim with one token per row")
+    blob, offs = _token_blob(tokens)
+    _check(lib().fw2v_write_embeddings(_p(rows, C.c_float), rows.shape[0], rows.shape[1], C.c_int64(rows.shape[1]),
+                                       blob, _p(offs, C.c_uint64), os.fsencode(path), threads))
+
+
 class Corpus:
     """Pre-subsampling corpus: vocabulary counts (id order), sentence offsets, ids."""
 
@@ -338,6 +356,14 @@ class Trainer:
 
     def init_model(self, seed):
         _check(lib().fw2v_init_model(self._h, C.c_uint64(seed)))
+
+    def save_model(self, path, tokens, which="input", threads=0):
+        """save_embeddings (model.cpp:47-74) of the device model; which: input | output."""
+        if len(tokens) != self.vocab:
+            raise ValueError("one token per vocabulary id")
+        blob, offs = _token_blob(tokens)
+        _check(lib().fw2v_save_model(self._h, {"input": 0, "output": 1}[which], blob, _p(offs, C.c_uint64),
+                                     os.fsencode(path), threads))
 
     def model_device(self):
         s0, s1, st = C.c_void_p(), C.c_void_p(), C.c_int32()
