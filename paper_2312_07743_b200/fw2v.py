@@ -44,7 +44,7 @@ EXPORTED = [
     "fw2v_train_corpus", "fw2v_train_sentences", "fw2v_plan_epoch", "fw2v_plan_info",
     "fw2v_plan_run", "fw2v_plan_destroy", "fw2v_keep_probs", "fw2v_table_build",
     "fw2v_assemble_batch", "fw2v_lr_at", "fw2v_analytic_traffic", "fw2v_corpus_synth_zipf",
-    "fw2v_corpus_view", "fw2v_corpus_free",
+    "fw2v_corpus_view", "fw2v_corpus_free", "fw2v_write_embeddings", "fw2v_save_model",
 ]
 
 
