@@ -43,6 +43,10 @@ $(BUILD)/fw2v_host.o: $(SRC)/fw2v_host.cpp include/fw2v.h $(SRC)/fw2v_device.cuh
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -c -o $@ $<
 
+$(BUILD)/fw2v_eval.o: $(SRC)/fw2v_eval.cu include/fw2v.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(BUILD)/ptxas_eval.log || (cat $(BUILD)/ptxas_eval.log; false)
+
 $(BUILD)/fw2v_io.o: $(SRC)/fw2v_io.cpp include/fw2v.h
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -O3 -c -o $@ $<
@@ -52,7 +56,7 @@ $(BUILD)/fw2v_corpus.o: $(SRC)/fw2v_corpus.cpp include/fw2v.h
 	$(CXX) $(CXXFLAGS) -O3 -c -o $@ $<
 
 $(LIB)/libfw2v.so: $(BUILD)/fw2v_kernels.o $(BUILD)/fw2v_snapshot.o $(K1S_OBJS) $(BUILD)/fw2v_host.o $(BUILD)/fw2v_corpus.o \
-                   $(BUILD)/fw2v_io.o
+                   $(BUILD)/fw2v_io.o $(BUILD)/fw2v_eval.o
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread -ldl -lrt
 

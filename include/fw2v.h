@@ -33,6 +33,8 @@ enum fw2v_status {
     FW2V_ERR_EMPTY_VOCAB = 3,
     FW2V_ERR_BAD_ARGUMENT = 4,
     FW2V_ERR_BAD_CONFIG = 5,
+    FW2V_ERR_OOV_QUERY = 11,
+    FW2V_ERR_ZERO_VECTOR = 12,
     FW2V_ERR_CUDA = 64,        /* CUDA runtime failure (message has the CUDA error string) */
     FW2V_ERR_UNSUPPORTED = 65, /* shape the B200 kernels do not cover (e.g. W_f > 5 on K1) */
     FW2V_ERR_NO_DEVICE = 66    /* no CUDA device: there is no CPU fallback by design */
@@ -216,6 +218,21 @@ int fw2v_write_embeddings(const float* rows, int32_t vocab_size, int32_t dim, in
 /* The same straight from a trainer's device model: which = 0 input (syn0), 1 output (syn1). */
 int fw2v_save_model(fw2v_ctx* ctx, int32_t which, const char* tokens, const uint64_t* token_offsets,
                     const char* path, int32_t threads);
+
+/* GPU evaluation scans, same arithmetic as the reference
+ * (double sums of float products in column order, no FMA) so the answers are
+ * identical. rows: |V| x dim host floats (e.g. LoadedEmbeddings::vectors).
+ * nearest_neighbors (eval.cpp:303-348) for n_queries ids at once: top-k
+ * (k <= 32) by cosine, query excluded, zero rows skipped, ties by id;
+ * out_ids/out_cos n_queries x k (-1 / NaN past the candidates). Errors:
+ * BAD_ARGUMENT (k not in [1, |V|-1]), OOV_QUERY, ZERO_VECTOR (zero query). */
+int fw2v_nearest_neighbors(const float* rows, int32_t vocab_size, int32_t dim, const int32_t* queries,
+                           int32_t n_queries, int32_t k, int32_t* out_ids, double* out_cos);
+/* eval_analogy's solve (eval.cpp:212-268) per quadruple (a, a*, b, b*) of ids:
+ * out_pred = argmax over x not in {a, a*, b} of the method's score on unit rows
+ * (0 cos_add, 1 cos_mul), first (lowest) id among equal maxima. */
+int fw2v_eval_analogy(const float* rows, int32_t vocab_size, int32_t dim, const int32_t* quads, int32_t n,
+                      int32_t method, int32_t* out_pred);
 
 /* Synthetic Zipf corpus of the benchmark shapes (bench
  * input, not the training path): `tokens` i.i.d. ranks r in 1..types with

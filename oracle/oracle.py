@@ -144,6 +144,28 @@ class Oracle:
                                                 rows.shape[1], rows.ctypes.data_as(C.POINTER(C.c_float)), which,
                                                 os.fsencode(str(path))))
 
+    def nearest_neighbors(self, rows, queries, k):
+        """Reference nearest_neighbors per query id -> (ids, cos), ref only."""
+        rows = np.ascontiguousarray(rows, np.float32)
+        q = np.ascontiguousarray(queries, np.int32)
+        ids = np.zeros((len(q), k), np.int32)
+        cos = np.zeros((len(q), k), np.float64)
+        self._check(self._fn("nearest_neighbors")(rows.ctypes.data_as(C.POINTER(C.c_float)), rows.shape[0],
+                                                  rows.shape[1], q.ctypes.data_as(C.POINTER(C.c_int32)), len(q), k,
+                                                  ids.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  cos.ctypes.data_as(C.POINTER(C.c_double))))
+        return ids, cos
+
+    def analogy_correct(self, rows, quads, method):
+        """Reference eval_analogy on each quadruple alone: 1 where it predicts quads[:, 3]."""
+        rows = np.ascontiguousarray(rows, np.float32)
+        qd = np.ascontiguousarray(quads, np.int32)
+        out = np.zeros(len(qd), np.int32)
+        self._check(self._fn("analogy_correct")(rows.ctypes.data_as(C.POINTER(C.c_float)), rows.shape[0],
+                                                rows.shape[1], qd.ctypes.data_as(C.POINTER(C.c_int32)), len(qd),
+                                                method, out.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out
+
     # -- scalar helpers ------------------------------------------------------
     def sigmoid(self, x: float) -> float:
         return self._fn("sigmoid")(x)

@@ -17,6 +17,8 @@
 //   ref_rng_draws        -> ringvec::Rng::derive/next_u64  rng.hpp:16-28
 //   ref_analytic_traffic -> ringvec::analytic_traffic      traffic.cpp:21
 //   ref_save_embeddings  -> ringvec::save_embeddings       model.cpp:47-74
+//   ref_nearest_neighbors-> ringvec::nearest_neighbors     eval.cpp:303-348
+//   ref_analogy_correct  -> ringvec::eval_analogy          eval.cpp:212-290
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -27,6 +29,7 @@
 #include "ringvec/config.hpp"
 #include "ringvec/corpus.hpp"
 #include "ringvec/error.hpp"
+#include "ringvec/eval.hpp"
 #include "ringvec/model.hpp"
 #include "ringvec/rng.hpp"
 #include "ringvec/sampler.hpp"
@@ -335,6 +338,54 @@ int ref_save_embeddings(const uint64_t* counts, int32_t vocab_size, int32_t dim,
         return 0;
     } catch (const std::exception& e) {
         return fail(e);
+    }
+}
+
+LoadedEmbeddings loaded(const float* rows, int32_t n, int32_t dim) {
+    LoadedEmbeddings e;
+    e.count = n;
+    e.dim = dim;
+    e.vectors.assign(rows, rows + static_cast<size_t>(n) * dim);
+    for (int32_t w = 0; w < n; ++w) {
+        e.tokens.push_back(token_name(w));
+        e.index[e.tokens.back()] = w;
+    }
+    return e;
+}
+
+// nearest_neighbors for query ids; out_ids/out_cos: n_queries x k (ids via the token names).
+int ref_nearest_neighbors(const float* rows, int32_t n, int32_t dim, const int32_t* queries, int32_t n_queries,
+                          int32_t k, int32_t* out_ids, double* out_cos) {
+    try {
+        LoadedEmbeddings e = loaded(rows, n, dim);
+        for (int32_t q = 0; q < n_queries; ++q) {
+            std::vector<Neighbor> nb = nearest_neighbors(e, token_name(queries[q]), k);
+            for (int32_t j = 0; j < k; ++j) {
+                const bool ok = j < static_cast<int32_t>(nb.size());
+                out_ids[static_cast<size_t>(q) * k + j] = ok ? e.id_of(nb[static_cast<size_t>(j)].token) : -1;
+                out_cos[static_cast<size_t>(q) * k + j] = ok ? nb[static_cast<size_t>(j)].cosine : 0.0;
+            }
+        }
+        return 0;
+    } catch (const std::exception& ex) {
+        return fail(ex);
+    }
+}
+
+// eval_analogy on each quadruple alone: correct[i] = 1 if the reference predicts quads[4i+3].
+int ref_analogy_correct(const float* rows, int32_t n, int32_t dim, const int32_t* quads, int32_t nq, int32_t method,
+                        int32_t* correct) {
+    try {
+        LoadedEmbeddings e = loaded(rows, n, dim);
+        for (int32_t i = 0; i < nq; ++i) {
+            std::vector<AnalogyQuadruple> one{{token_name(quads[4 * i]), token_name(quads[4 * i + 1]),
+                                               token_name(quads[4 * i + 2]), token_name(quads[4 * i + 3])}};
+            AnalogyResult r = eval_analogy(e, one, method == 0 ? AnalogyMethod::cos_add : AnalogyMethod::cos_mul, 1);
+            correct[i] = r.accuracy == 1.0 ? 1 : 0;
+        }
+        return 0;
+    } catch (const std::exception& ex) {
+        return fail(ex);
     }
 }
 

@@ -49,6 +49,7 @@ cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& 
 bool k1s_supported(int lanes, int vec, int n_neg, int wf);
 int write_embeddings(const float* rows, int32_t vocab_size, int32_t dim, int64_t row_stride, const char* tokens,
                      const uint64_t* token_offsets, const char* path, int32_t threads, std::string* err);
+void set_last_error(const std::string& msg);
 } // namespace fw2v
 
 namespace {
@@ -1360,3 +1361,7 @@ int fw2v_analytic_traffic(uint64_t length, int32_t width, int32_t negatives, int
 }
 
 } // extern "C"
+
+namespace fw2v {
+void set_last_error(const std::string& msg) { g_error = msg; }
+} // namespace fw2v

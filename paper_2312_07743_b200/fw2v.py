@@ -45,6 +45,7 @@ EXPORTED = [
     "fw2v_plan_run", "fw2v_plan_destroy", "fw2v_keep_probs", "fw2v_table_build",
     "fw2v_assemble_batch", "fw2v_lr_at", "fw2v_analytic_traffic", "fw2v_corpus_synth_zipf",
     "fw2v_corpus_view", "fw2v_corpus_free", "fw2v_write_embeddings", "fw2v_save_model",
+    "fw2v_nearest_neighbors", "fw2v_eval_analogy",
 ]
 
 
@@ -267,6 +268,27 @@ def write_embeddings(path, rows, tokens, threads=0):
     blob, offs = _token_blob(tokens)
     _check(lib().fw2v_write_embeddings(_p(rows, C.c_float), rows.shape[0], rows.shape[1], C.c_int64(rows.shape[1]),
                                        blob, _p(offs, C.c_uint64), os.fsencode(path), threads))
+
+
+def nearest_neighbors(rows, queries, k):
+    """nearest_neighbors (eval.cpp:303-348) on the GPU for many query ids: (ids, cos), each |Q| x k."""
+    rows = np.ascontiguousarray(rows, np.float32)
+    q = np.ascontiguousarray(queries, np.int32)
+    ids = np.zeros((len(q), k), np.int32)
+    cos = np.zeros((len(q), k), np.float64)
+    _check(lib().fw2v_nearest_neighbors(_p(rows, C.c_float), rows.shape[0], rows.shape[1], _p(q, C.c_int32), len(q), k,
+                                        _p(ids, C.c_int32), _p(cos, C.c_double)))
+    return ids, cos
+
+
+def eval_analogy(rows, quads, method="cos_add"):
+    """eval_analogy (eval.cpp:212-290) on the GPU: (predicted ids, accuracy) for |Q| x 4 id quadruples."""
+    rows = np.ascontiguousarray(rows, np.float32)
+    qd = np.ascontiguousarray(quads, np.int32).reshape(-1, 4)
+    pred = np.zeros(len(qd), np.int32)
+    _check(lib().fw2v_eval_analogy(_p(rows, C.c_float), rows.shape[0], rows.shape[1], _p(qd, C.c_int32), len(qd),
+                                   {"cos_add": 0, "cos_mul": 1}[method], _p(pred, C.c_int32)))
+    return pred, float((pred == qd[:, 3]).mean()) if len(qd) else 0.0
 
 
 class Corpus:
