@@ -36,6 +36,7 @@ struct ModelView {
     float* hot;
     int32_t hot_k;
     int32_t hot_r;
+    int32_t hot_row;  // (hot - syn1) / (stride floats): replica r of row id is syn1 row hot_row + r*hot_k + id
 };
 
 // K1s memory-path options.

@@ -380,6 +380,11 @@ uint64_t assemble(const CorpusView& c, uint64_t& cursor, uint64_t end, uint64_t 
     return kept;
 }
 
+// Negative arrays on the device carry this much zeroed padding: the K1s kernel
+// reads the negatives of a position as one fixed-size group (immediate offsets,
+// no clamping), which may run past the last position's N values.
+constexpr size_t kNegPadBytes = 64;
+
 // ------------------------------------------------------------ K1 shapes
 struct Shape {
     int lanes = 0, vec = 0;
@@ -503,8 +508,29 @@ struct fw2v_ctx {
     int32_t k1_flags = 0;
     int64_t inflight_total = 0;  // Hogwild sentences in flight over all streams (0 = unlimited)
     float* hot = nullptr;        // hot-row replicas, hot_r x hot_k x stride (K1s Hogwild only)
+    float* hot_alloc = nullptr;  // allocation holding `hot` (one spare row for alignment)
     int32_t hot_k = 0, hot_r = 1;
-    ModelView model_view() const { return ModelView{syn0, syn1, cfg.dim, stride, vocab, k1_flags, hot, hot_k, hot_r}; }
+    int64_t hot_row = 0;         // (hot - syn1) in rows: the kernel addresses replicas from syn1
+    // Places the replicas a whole number of rows from syn1 (the kernel forms a
+    // 32-bit row index and one pointer); disables them if that is impossible.
+    void place_hot() {
+        if (hot_alloc == nullptr) return;
+        const int64_t row = static_cast<int64_t>(sizeof(float)) * stride;
+        const int64_t diff = reinterpret_cast<int64_t>(hot_alloc) - reinterpret_cast<int64_t>(syn1);
+        int64_t rows_off = diff / row;
+        while (rows_off * row < diff) ++rows_off;  // first whole-row position inside the allocation
+        hot = reinterpret_cast<float*>(reinterpret_cast<char*>(syn1) + rows_off * row);
+        hot_row = rows_off;
+        const int64_t last = rows_off + static_cast<int64_t>(hot_k) * hot_r;
+        if (rows_off < INT32_MIN / 2 || last > INT32_MAX / 2) {  // outside a 32-bit row range: plain Hogwild
+            hot_k = 0;
+            hot = nullptr;
+            hot_row = 0;
+        }
+    }
+    ModelView model_view() const {
+        return ModelView{syn0, syn1, cfg.dim, stride, vocab, k1_flags, hot, hot_k, hot_r, static_cast<int32_t>(hot_row)};
+    }
     // Around every Hogwild pass: replicas <- syn1 before, syn1 <- mean(replicas) after.
     void hot_sync(bool average, cudaStream_t st) const { FW2V_CK(launch_hot_sync(model_view(), average, st)); }
 
@@ -590,7 +616,7 @@ struct fw2v_ctx {
                 FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_off), 4 * (cap_sent + 1), cudaHostAllocDefault));
                 FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_alpha), 4 * cap_sent, cudaHostAllocDefault));
                 FW2V_CK(cudaMalloc(&s.d_ids, 4 * cap_words));
-                FW2V_CK(cudaMalloc(&s.d_negs, 4 * cap_words * nn));
+                FW2V_CK(cudaMalloc(&s.d_negs, 4 * cap_words * nn + kNegPadBytes));
                 FW2V_CK(cudaMalloc(&s.d_off, 4 * (cap_sent + 1)));
                 FW2V_CK(cudaMalloc(&s.d_alpha, 4 * cap_sent));
                 FW2V_CK(cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming));
@@ -608,7 +634,7 @@ struct fw2v_ctx {
             cudaFree(ln.d_ctr);
             if (ln.stream) cudaStreamDestroy(ln.stream);
         }
-        cudaFree(hot);
+        cudaFree(hot_alloc);
         if (own_model) {
             cudaFree(syn0);
             cudaFree(syn1);
@@ -775,7 +801,8 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         if (!x->deterministic && cfg->reuse_mode == kWindowSnapshot && x->k1s_shape.lanes > 0 && cfg->hot_rows > 0) {
             x->hot_k = std::min(cfg->hot_rows, vocab_size);
             x->hot_r = cfg->hot_replicas;
-            FW2V_CK(cudaMalloc(&x->hot, sizeof(float) * static_cast<size_t>(x->hot_k) * x->hot_r * x->stride));
+            FW2V_CK(cudaMalloc(&x->hot_alloc, sizeof(float) * (static_cast<size_t>(x->hot_k) * x->hot_r + 1) * x->stride));
+            x->place_hot();
             x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
                                 : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives,
                                                                          cfg->alpha0, x->hot_k, x->hot_r)
@@ -871,6 +898,7 @@ int fw2v_attach_model(fw2v_ctx* x, float* syn0, float* syn1) {
         x->syn0 = syn0;
         x->syn1 = syn1;
         x->own_model = false;
+        x->place_hot();  // replicas are addressed relative to syn1
     });
 }
 
@@ -892,7 +920,7 @@ int fw2v_train_sentences(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_senten
             ~Free() { for (void* q : p) cudaFree(q); }
         } guard{{nullptr, nullptr, nullptr, nullptr, nullptr}};
         FW2V_CK(cudaMalloc(&d_ids, 4 * std::max<uint64_t>(words, 1))); guard.p[0] = d_ids;
-        FW2V_CK(cudaMalloc(&d_negs, 4 * std::max<uint64_t>(words * n, 1))); guard.p[1] = d_negs;
+        FW2V_CK(cudaMalloc(&d_negs, 4 * std::max<uint64_t>(words * n, 1) + kNegPadBytes)); guard.p[1] = d_negs;
         FW2V_CK(cudaMalloc(&d_off, 4 * (n_sentences + 1))); guard.p[2] = d_off;
         FW2V_CK(cudaMalloc(&d_alpha, 4 * std::max<uint64_t>(n_sentences, 1))); guard.p[3] = d_alpha;
         FW2V_CK(cudaMalloc(&d_ctr, sizeof(DevCounters))); guard.p[4] = d_ctr;
@@ -1183,6 +1211,7 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
                     HostBatch hb;
                     hb.ids.assign(bi.begin(), bi.begin() + static_cast<ptrdiff_t>(words));
                     hb.negs.assign(bn.begin(), bn.begin() + static_cast<ptrdiff_t>(words * n_neg));
+                    hb.negs.resize(hb.negs.size() + kNegPadBytes / 4, 0);  // kernels read a window's row whole
                     hb.off.assign(bo.begin(), bo.begin() + static_cast<ptrdiff_t>(kept + 1));
                     const uint64_t base = reserved.fetch_add(words);
                     hb.alpha.resize(kept);

@@ -281,9 +281,11 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     float* __restrict__ syn0 = m.syn0 + sub * SL::CW;
     float* __restrict__ syn1 = m.syn1 + sub * SL::CW;
     // Output row of sample s >= 0: hot rows go to this sentence's replica.
-    float* const hot_base = m.hot_k > 0 ? m.hot + (sent % m.hot_r) * m.hot_k * STRIDE + sub * SL::CW : syn1;
+    // Output row of sample s >= 0 as one row index from syn1: hot rows go to this
+    // sentence's replica (ModelView::hot_row), one select instead of two bases.
     const int hot_k = m.hot_k;
-    auto srow = [&](int s) { return (s < hot_k ? hot_base : syn1) + s * STRIDE; };
+    const int hot_off = m.hot_k > 0 ? m.hot_row + (sent % m.hot_r) * m.hot_k : 0;
+    auto srow = [&](int s) { return syn1 + static_cast<int64_t>(s < hot_k ? s + hot_off : s) * STRIDE; };
     const int tail = L - C;  // positions >= tail stay resident until finish()
 
     // After the butterfly, slot j of this lane holds dot idx = q*NCTX + r. One

@@ -70,7 +70,17 @@ int main(int argc, char** argv) {
         CK(cudaMalloc(&dhot, sizeof(float) * KB_HOT_K * KB_HOT_R * STRIDE));
         CK(cudaMemset(dhot, 0, sizeof(float) * KB_HOT_K * KB_HOT_R * STRIDE));
     }
-    fw2v::ModelView m{d0, d1, D, STRIDE, V, KB_FLAGS, dhot, KB_HOT_K, KB_HOT_R};
+    int hot_row = 0;
+    if (dhot) {  // replicas addressed from syn1 by a whole row offset (as fw2v_host.cpp places them)
+        CK(cudaFree(dhot));
+        CK(cudaMalloc(&dhot, sizeof(float) * (KB_HOT_K * KB_HOT_R + 1) * STRIDE));
+        const long long row = 4LL * STRIDE, diff = (long long)((char*)dhot - (char*)d1);
+        long long r = diff / row; while (r * row < diff) ++r;
+        hot_row = (int)r;
+        CK(cudaMemset((char*)d1 + r * row, 0, sizeof(float) * KB_HOT_K * KB_HOT_R * STRIDE));
+        dhot = (float*)((char*)d1 + r * row);
+    }
+    fw2v::ModelView m{d0, d1, D, STRIDE, V, KB_FLAGS, dhot, KB_HOT_K, KB_HOT_R, hot_row};
     std::vector<cudaStream_t> ss(chunks);
     for (auto& s : ss) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
