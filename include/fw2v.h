@@ -76,9 +76,12 @@ typedef struct fw2v_config {
                                 SM's L1 every window (exact per-sentence order); k > 0 = one warp per
                                 block refreshes the L1 every 2^k windows (bounded staleness for
                                 Zipf-hot rows) */
-    int32_t delta_writeback; /* Hogwild kernels: 1 = rows leave the ring / sweep as red.add(final -
-                                loaded) so concurrent sentences never overwrite each other's updates;
-                                0 = overwrite, the reference's per-sentence write sequence exactly */
+    int32_t delta_writeback; /* Hogwild write-back of ring (context) rows: 2 = stored straight back
+                                when they leave the ring (Hogwild overwrite like the reference's
+                                memcpy, K1s keeps no shared-memory ring: the fastest, default);
+                                1 = red.add(final - loaded): concurrent sentences never overwrite
+                                each other's updates; 0 = overwrite in the reference's exact
+                                per-sentence order (finish() slot order; exactness tests) */
     int32_t max_inflight;  /* Hogwild: sentences in flight on the device at once, summed over the
                               streams. 0 = auto (collision budget from the vocabulary, see DESIGN.md
                               §5), -1 = unlimited (every sentence of a batch in one launch) */

@@ -440,6 +440,7 @@ void validate(const fw2v_config& c) {  // validate_config (config.cpp:165-177)
     if (c.reuse_mode < 0 || c.reuse_mode > 3) fail(FW2V_ERR_BAD_CONFIG, "unknown reuse mode");
     if (c.sampler < 0 || c.sampler > 1) fail(FW2V_ERR_BAD_CONFIG, "unknown sampler");
     if (c.hot_rows < 0 || c.hot_replicas < 1) fail(FW2V_ERR_BAD_CONFIG, "hot_rows must be >= 0 and hot_replicas >= 1");
+    if (c.delta_writeback < 0 || c.delta_writeback > 2) fail(FW2V_ERR_BAD_CONFIG, "delta_writeback must be 0, 1 or 2");
 }
 
 void require_device(int device) {
@@ -735,7 +736,7 @@ void fw2v_config_default(fw2v_config* c) {
     c->k1_lanes = 0;
     c->streams = 0;
     c->l1_refresh_log2 = 5;
-    c->delta_writeback = 1;
+    c->delta_writeback = 2;
     c->max_inflight = 0;
     c->hot_rows = 64;
     c->hot_replicas = 16;
@@ -772,7 +773,10 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         x->vocab = vocab_size;
         // Sample rows are always written as red.global.add of the window delta
         // (row += delta, trainer.cpp:198-204); reads optionally go through L1.
-        x->k1_flags = kFlagRedSamples | (cfg->delta_writeback ? kFlagDeltaRing : 0);
+        // delta_writeback: 1 red.add(final - loaded); 2 K1s stores ring rows straight
+        // back (no shared-memory ring; K1 treats it as 1); 0 reference overwrite order.
+        x->k1_flags = kFlagRedSamples | (cfg->delta_writeback != 0 ? kFlagDeltaRing : 0) |
+                      (cfg->delta_writeback == 2 ? kFlagNoRing : 0);
         x->k1_flags |= cfg->l1_refresh_log2 > 0 ? (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift) : kFlagL1Exact;
         if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments
         x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight

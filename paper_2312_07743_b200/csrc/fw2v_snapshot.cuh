@@ -97,7 +97,7 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 constexpr int kPrefetchWindows = 16;
 
-template <int LANES, int VEC, int WF, int NC>
+template <int LANES, int VEC, int WF, int NC, bool RING = true>
 struct K1sSmem {
     static constexpr int NCTX = 2 * WF;
     static constexpr int C = 2 * WF + 1;
@@ -110,10 +110,12 @@ struct K1sSmem {
     // Per group (one sentence): the window's g coefficients (scalars), the
     // sample rows double-buffered by window parity, and the ring rows as loaded
     // (delta write-back) or the finish() stash (overwrite) — never both.
-    static constexpr int kGroupFloats = GPAD + 2 * NC * STRIDE + C * STRIDE;
+    // RING = false (Hogwild overwrite write-back): ring rows leave straight to HBM,
+    // no shared-memory ring: 64% of the footprint, 6 blocks per SM at d=128.
+    static constexpr int kGroupFloats = GPAD + 2 * NC * STRIDE + (RING ? C * STRIDE : 0);
     static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
-    static constexpr int kRegBlocks = VEC >= 8 ? 5 : 3;
+    static constexpr int kRegBlocks = VEC >= 8 ? (RING ? 5 : 6) : 3;
     static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
 };
 
@@ -229,11 +231,23 @@ struct Slice {
     }
 };
 
-template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
-__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC>::THREADS, K1sSmem<LANES, VEC, WF, NC>::MINB)
-k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) {
+// MODE: kFullChunk (N + 1 == NC samples, one chunk: every per-sample validity
+// test is compile-time), kPartChunk (N + 1 < NC), kMultiChunk (N + 1 > NC:
+// chunks of NC samples loaded per window).
+constexpr int kFullChunk = 0, kPartChunk = 1, kMultiChunk = 2;
+
+// RING: the ring rows' shared-memory copy (entry values for the delta
+// write-back, or the finish() stash for the exact overwrite order). Without it
+// rows leaving the ring are stored straight back (Hogwild overwrite, the
+// reference's memcpy write-back, trainer.cpp:61-63, in any finish order).
+template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true>
+__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC, RING>::THREADS, K1sSmem<LANES, VEC, WF, NC, RING>::MINB)
+k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ ctr) {
     static_assert(VEC % 2 == 0, "K1s stages 8- or 16-byte chunks");
-    using SM = K1sSmem<LANES, VEC, WF, NC>;
+    constexpr bool MULTI = MODE == kMultiChunk;
+    constexpr bool FULL = MODE == kFullChunk;
+    const int n_neg = FULL ? NC - 1 : n_neg_arg;  // compile-time on the full-chunk path
+    using SM = K1sSmem<LANES, VEC, WF, NC, RING>;
     constexpr int NCTX = SM::NCTX;
     constexpr int C = SM::C;
     constexpr int NV = SM::NV;
@@ -262,7 +276,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
     float* sbuf = gsh + SM::GPAD + sub * SL::CW;                  // + (parity*NC + q)*STRIDE
     float* ring = gsh + SM::GPAD + 2 * NC * STRIDE + sub * SL::CW;  // + slot*STRIDE
-    const bool delta_wb = (m.flags & kFlagDeltaRing) != 0;
+    const bool delta_wb = RING && (m.flags & kFlagDeltaRing) != 0;
 
     uint32_t beg = 0, len = 0;
     float alpha = 0.0f;
@@ -367,13 +381,14 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     }
     float2 dctx[MULTI ? NCTX : 1][H2];
 
+    unsigned vmask = 0;  // bit r: context slot r holds a position of the sentence
+#pragma unroll
+    for (int r = 0; r < NCTX; ++r) vmask |= (tok[r] >= 0 ? 1u : 0u) << r;
+
     KB_T_DECL
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
         const bool wact = act && L >= 2;
-        unsigned vmask = 0;
-#pragma unroll
-        for (int r = 0; r < NCTX; ++r) vmask |= (tok[r] >= 0 ? 1u : 0u) << r;
         const int q_in = i + 1 + WF;
         // Token ids run one window ahead of their rows and negatives two; loads
         // issued early are carried raw and masked where consumed. The
@@ -450,7 +465,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
                 int s;
                 if constexpr (MULTI) s = (kk == 0) ? ttok : (wact && kk <= n_neg ? __ldg(negs + i * n_neg + kk - 1) : -1);
                 else s = q == 0 ? ttok : ncur[q > 0 ? q - 1 : 0];
-                sid[q] = (wact && kk <= n_neg) ? s : -1 - q;  // empty slots: distinct negative ids
+                // Empty slots: distinct negative ids. On the full-chunk path every
+                // slot holds a valid id whenever the window is active.
+                if constexpr (FULL) sid[q] = s;
+                else sid[q] = (wact && kk <= n_neg) ? s : -1 - q;
             }
             const float* cur = sbuf;
             if constexpr (!MULTI) {
@@ -463,7 +481,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
                 if (stale != 0u) {
 #pragma unroll
                     for (int q = 0; q < NC; ++q)
-                        if (((stale >> q) & 1u) && sid[q] >= 0) {
+                        if (((stale >> q) & 1u) && (FULL ? wact : sid[q] >= 0)) {
                             float2 v[H2];
                             SL::load(v, srow(sid[q]));
                             SL::store_shared(const_cast<float*>(cur) + q * STRIDE, v);
@@ -541,7 +559,8 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 #pragma unroll
                     for (int h = 0; h < H2; ++h)
                         D[h] = __ffma2_rn(make_float2(g[q * NCTX + r], g[q * NCTX + r]), ctx[r][h], D[h]);
-                SL::red_add_if(sid[q] >= 0, srow(max(sid[q], 0)), D);
+                if constexpr (FULL) SL::red_add_if(wact, srow(sid[q]), D);
+                else SL::red_add_if(sid[q] >= 0, srow(max(sid[q], 0)), D);
             }
             KB_T(6)
             // 4b. context rows from window-entry sample rows.
@@ -577,7 +596,9 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         const int etok = tok[0];
         if (etok >= 0) {
             const int p = i - WF;
-            if (delta_wb) {
+            if (!RING) {
+                SL::store(syn0 + etok * STRIDE, ctx[0]);
+            } else if (delta_wb) {
                 SL::red_delta(syn0 + etok * STRIDE, ctx[0], ring + (p % C) * STRIDE);
             } else if (p >= tail) {
                 SL::store_shared(ring + (p % C) * STRIDE, ctx[0]);
@@ -597,6 +618,9 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
         for (int r = WF; r < NCTX - 1; ++r) { vcopy2(ctx[r], ctx[r + 1]); tok[r] = tok[r + 1]; }
         vcopy2(ctx[NCTX - 1], inc);
         tok[NCTX - 1] = inc_tok;
+        // The validity mask slides with the slots: bit WF-1 takes the old target.
+        vmask = ((vmask >> 1) & ~(1u << (WF - 1))) | ((act && tok[WF - 1] >= 0 ? 1u : 0u) << (WF - 1)) |
+                ((inc_tok >= 0 ? 1u : 0u) << (NCTX - 1));
         if constexpr (!MULTI) {
 #pragma unroll
             for (int k = 0; k < NN; ++k) ncur[k] = nnext[k];
@@ -617,7 +641,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
     KB_T_DUMP
     // ContextRing::finish (trainer.cpp:71-75): residents in slot order.
     const int i_end = Lmax;  // registers hold positions i_end-WF .. i_end+WF
-    if (delta_wb) {
+    if (!RING) {
+#pragma unroll
+        for (int r = 0; r < NCTX; ++r)
+            if (tok[r] >= 0) SL::store(syn0 + tok[r] * STRIDE, ctx[r]);
+        if (ttok >= 0) SL::store(syn0 + ttok * STRIDE, tgt);
+    } else if (delta_wb) {
         // Deltas commute: no ordering to preserve.
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) {
@@ -665,36 +694,43 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr)
 }
 
 // ------------------------------------------------------------------ dispatch
-template <int LANES, int VEC, int WF, int NC, bool MULTI, bool FAST>
+template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true>
 cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, int n_neg, DevCounters* ctr,
                             cudaStream_t st, int* resident) {
-    constexpr int bytes = K1sSmem<LANES, VEC, WF, NC>::kBlockBytes;
-    auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MULTI, FAST>;
+    using SMx = K1sSmem<LANES, VEC, WF, NC, RING>;
+    constexpr int bytes = SMx::kBlockBytes;
+    auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MODE, FAST, RING>;
     static bool configured = false;  // benign race: idempotent attribute set
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    constexpr int threads = K1sSmem<LANES, VEC, WF, NC>::THREADS;
+    constexpr int threads = SMx::THREADS;
     if (resident != nullptr) return resident_sentences(kern, bytes, threads, threads / LANES, resident);
     if (blocks == 0) return cudaSuccess;
-    kern<<<blocks, K1sSmem<LANES, VEC, WF, NC>::THREADS, bytes, st>>>(m, b, n_neg, ctr);
+    kern<<<blocks, threads, bytes, st>>>(m, b, n_neg, ctr);
     return cudaGetLastError();
 }
 
 template <int LANES, int VEC, int WF, int NC>
 cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
                           cudaStream_t st, int* resident) {
-    constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;
+    constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;  // RING does not change THREADS
     const int blocks = (b.n_sentences + per_block - 1) / per_block;
-    const bool multi = n_neg + 1 > NC;
-    if (multi) {
-        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, true, true>(blocks, m, b, n_neg, ctr, st, resident)
-                    : launch_k1s_inst<LANES, VEC, WF, NC, true, false>(blocks, m, b, n_neg, ctr, st, resident);
+    if (n_neg + 1 > NC)
+        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true>(blocks, m, b, n_neg, ctr, st, resident)
+                    : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false>(blocks, m, b, n_neg, ctr, st, resident);
+    // Hogwild overwrite (no shared-memory ring) is built for the fast sigmoid only.
+    const bool no_ring = fast && (m.flags & kFlagNoRing) != 0;
+    if (n_neg + 1 < NC) {
+        if (no_ring) return launch_k1s_inst<LANES, VEC, WF, NC, kPartChunk, true, false>(blocks, m, b, n_neg, ctr, st, resident);
+        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kPartChunk, true>(blocks, m, b, n_neg, ctr, st, resident)
+                    : launch_k1s_inst<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, ctr, st, resident);
     }
-    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, false, true>(blocks, m, b, n_neg, ctr, st, resident)
-                : launch_k1s_inst<LANES, VEC, WF, NC, false, false>(blocks, m, b, n_neg, ctr, st, resident);
+    if (no_ring) return launch_k1s_inst<LANES, VEC, WF, NC, kFullChunk, true, false>(blocks, m, b, n_neg, ctr, st, resident);
+    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, ctr, st, resident)
+                : launch_k1s_inst<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, ctr, st, resident);
 }
 
 template <int LANES, int VEC>

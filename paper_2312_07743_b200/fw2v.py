@@ -125,7 +125,7 @@ class TrainConfig:
     k1_lanes: int = 0
     streams: int = 0
     l1_refresh_log2: int = 5
-    delta_writeback: bool = True
+    delta_writeback: int = 2  # 2 Hogwild overwrite (K1s: no smem ring), 1 red.add delta, 0 exact overwrite order
     max_inflight: int = 0
     hot_rows: int = 64
     hot_replicas: int = 16

@@ -227,3 +227,26 @@ def test_k1s_hot_replicas_average(oracle, replicas):
     want[:hot] = go0[:hot] + (ro[:hot] - go0[:hot]) / replicas
     assert np.abs(gi - ri).max() <= 2e-5 * np.abs(ri).max() + 1e-7
     assert np.abs(go - want).max() <= 2e-5 * np.abs(ro).max() + 1e-7
+
+
+@pytest.mark.parametrize("dim", [32, 64, 128, 300])
+def test_k1s_overwrite_without_ring_matches_delta(dim):
+    """delta_writeback=2 (ring rows stored straight back, no shared-memory ring;
+    fast-sigmoid kernels) equals the delta write-back on row-disjoint sentences
+    with distinct ring tokens, where neither can lose an update."""
+    n, L, n_neg, pool = 96, 40, 5, 48
+    counts, offsets, ids, negs = _disjoint_batch(n, L, pool, n_neg, seed=dim + 1, distinct=True)
+    V = len(counts)
+    alphas = np.full(n, 0.025, np.float32)
+    rng = np.random.default_rng(dim)
+    gi0 = ((rng.random((V, dim)) - 0.5) / dim).astype(np.float32)
+    go0 = ((rng.random((V, dim)) - 0.5) / dim).astype(np.float32)
+    out = {}
+    for mode in (1, 2):
+        with _trainer(counts=counts, dim=dim, window=5, negatives=n_neg, workers=4, reuse_mode="window_snapshot",
+                      deterministic=0, fast_sigmoid=True, hot_rows=0, l1_refresh_log2=0, delta_writeback=mode) as t:
+            t.set_model(gi0, go0)
+            t.train_sentences(offsets, ids, negs, alphas, serial=False)
+            out[mode] = t.get_model()
+    for a, b in zip(out[1], out[2]):
+        assert np.abs(a - b).max() <= 1e-6 * np.abs(a).max() + 1e-8
