@@ -204,6 +204,11 @@ int64_t fw2v_assemble_batch(const uint64_t* counts, int32_t vocab_size, const ui
                             uint64_t table_size, double threshold, uint64_t seed, uint64_t a,
                             uint64_t b, uint64_t c, int32_t* out_ids, uint64_t* out_offsets,
                             int32_t* out_negs);
+/* `count` draws of the alias sampler (unigram^power; the throughput-mode negative
+ * sampler) from the stream Rng::derive(seed, 0): AVX-512 when the host has it,
+ * else scalar; both give the same sequence. */
+int fw2v_alias_draws(const uint64_t* counts, int32_t vocab_size, double power, uint64_t seed, uint64_t count,
+                     int32_t* out);
 /* lr_at (model.cpp:39-45) */
 float fw2v_lr_at(uint64_t words_trained, uint64_t total, float alpha0);
 /* analytic_traffic (traffic.cpp:21-59) */

@@ -26,6 +26,9 @@
 #include <cstring>
 #include <ctime>
 #include <sys/mman.h>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 #include <memory>
 #include <mutex>
 #include <string>
@@ -313,16 +316,99 @@ struct BatchOut {
 // assemble_batch (sampler.cpp:41-63) + subsample_sentence (corpus.cpp:232-241):
 // same RNG consumption order, so the batch equals the reference's for the
 // same stream. Returns kept sentences; *words = their total length.
+// ---- AVX-512 batching kernels. Draw k (1-based) of a stream in state s is
+// mix64(s + k*golden) (Rng::next), so 8 consecutive draws are independent and
+// vectorise; results and the final stream state equal the scalar loops'.
+#if defined(__x86_64__)
+#define FW2V_AVX512 __attribute__((target("avx512f,avx512dq,avx512vl")))
+FW2V_AVX512 inline __m512i mix64x8(__m512i z) {
+    z = _mm512_mullo_epi64(_mm512_xor_si512(z, _mm512_srli_epi64(z, 30)), _mm512_set1_epi64(0xbf58476d1ce4e5b9LL));
+    z = _mm512_mullo_epi64(_mm512_xor_si512(z, _mm512_srli_epi64(z, 27)), _mm512_set1_epi64(0x94d049bb133111ebLL));
+    return _mm512_xor_si512(z, _mm512_srli_epi64(z, 31));
+}
+// Stream positions s + (k+1)*golden for k = 0..7, and the step to the next 8.
+FW2V_AVX512 inline __m512i stream8(uint64_t s) {
+    const __m512i k = _mm512_set_epi64(8, 7, 6, 5, 4, 3, 2, 1);
+    return _mm512_add_epi64(_mm512_set1_epi64(static_cast<long long>(s)),
+                            _mm512_mullo_epi64(k, _mm512_set1_epi64(static_cast<long long>(kGolden))));
+}
+// cnt alias draws (AliasTable::sample) into out; returns the advanced state.
+FW2V_AVX512 uint64_t alias_draws_avx512(uint64_t s, const AliasTable::Entry* E, uint32_t n, int32_t* out,
+                                        uint64_t cnt) {
+    const __m512i step = _mm512_set1_epi64(static_cast<long long>(8 * kGolden));
+    const __m512i nv = _mm512_set1_epi64(n);
+    const __m512i lo32 = _mm512_set1_epi64(0xffffffffLL);
+    __m512i pos = stream8(s);
+    uint64_t x = 0;
+    for (; x + 8 <= cnt; x += 8) {
+        const __m512i u = mix64x8(pos);
+        pos = _mm512_add_epi64(pos, step);
+        const __m512i col = _mm512_srli_epi64(_mm512_mul_epu32(u, nv), 32);  // (u32 * n) >> 32
+        const __m512i en = _mm512_i64gather_epi64(col, reinterpret_cast<const long long*>(E), 8);
+        const __mmask8 acc = _mm512_cmplt_epu64_mask(_mm512_srli_epi64(u, 32), _mm512_and_si512(en, lo32));
+        const __m512i v = _mm512_mask_blend_epi64(acc, _mm512_srli_epi64(en, 32), col);
+        _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + x), _mm512_cvtepi64_epi32(v));
+    }
+    s += x * kGolden;
+    for (; x < cnt; ++x) {
+        s += kGolden;
+        const uint64_t u = mix64(s);
+        const uint32_t col = static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(u)) * n) >> 32);
+        out[x] = static_cast<uint32_t>(u >> 32) < E[col].prob ? static_cast<int32_t>(col) : E[col].alias;
+    }
+    return s;
+}
+// Subsampling of ids[0..len) (corpus.cpp:232-241): keeps id when next_double() <
+// keep[id], in order; writes the kept ids to dst, returns their count.
+FW2V_AVX512 uint64_t subsample_avx512(uint64_t* state, const int32_t* ids, uint64_t len, const double* keep,
+                                      int32_t* dst) {
+    uint64_t s = *state;
+    const __m512i step = _mm512_set1_epi64(static_cast<long long>(8 * kGolden));
+    const __m512d scale = _mm512_set1_pd(0x1.0p-53);
+    __m512i pos = stream8(s);
+    uint64_t p = 0, n = 0;
+    for (; p + 8 <= len; p += 8) {
+        const __m512i u = mix64x8(pos);
+        pos = _mm512_add_epi64(pos, step);
+        const __m512d d = _mm512_mul_pd(_mm512_cvtepu64_pd(_mm512_srli_epi64(u, 11)), scale);
+        const __m256i id = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(ids + p));
+        const __m512d k = _mm512_i32gather_pd(id, keep, 8);
+        const __mmask8 m = _mm512_cmp_pd_mask(d, k, _CMP_LT_OQ);
+        _mm256_mask_compressstoreu_epi32(dst + n, m, id);
+        n += static_cast<uint64_t>(__builtin_popcount(m));
+    }
+    s += p * kGolden;
+    for (; p < len; ++p) {
+        s += kGolden;
+        const int32_t id = ids[p];
+        dst[n] = id;
+        n += static_cast<double>(mix64(s) >> 11) * 0x1.0p-53 < keep[id] ? 1 : 0;
+    }
+    *state = s;
+    return n;
+}
+bool have_avx512() {
+    static const bool on = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512dq") &&
+                           __builtin_cpu_supports("avx512vl") && std::getenv("FW2V_NO_AVX512") == nullptr;
+    return on;
+}
+#else
+bool have_avx512() { return false; }
+#endif
+
 uint64_t assemble(const CorpusView& c, uint64_t& cursor, uint64_t end, uint64_t max_sentences,
                   const Sampler& sp, Rng& rng, const BatchOut& out, uint64_t* words) {
     uint64_t kept = 0, w = 0;
     out.offsets[0] = 0;
     const int n_neg = sp.n_neg;
+    const bool vec = have_avx512();
     while (kept < max_sentences && cursor < end) {
         const uint64_t b = c.offsets[cursor], e = c.offsets[cursor + 1];
         if (w + (e - b) > out.cap_words) break;  // caller sized for the worst case; never hit
         const uint64_t start = w;
-        if (sp.keep != nullptr) {
+        if (sp.keep != nullptr && vec) {
+            w += subsample_avx512(&rng.state, c.ids + b, e - b, sp.keep, out.ids + w);
+        } else if (sp.keep != nullptr) {
             // One next_double per raw token, kept in order (corpus.cpp:232-241);
             // branch-free: keep decisions are coin flips for frequent words.
             int32_t* dst = out.ids + w;
@@ -344,7 +430,9 @@ uint64_t assemble(const CorpusView& c, uint64_t& cursor, uint64_t end, uint64_t 
         // The stream state and tables live in locals: through the references the
         // compiler must assume the int32 stores into ng may alias them.
         Rng r = rng;
-        if (sp.alias != nullptr) {
+        if (sp.alias != nullptr && vec) {
+            r.state = alias_draws_avx512(r.state, sp.alias->e.data(), sp.alias->n, ng, cnt);
+        } else if (sp.alias != nullptr) {
             const AliasTable::Entry* const E = sp.alias->e.data();
             const uint64_t n = sp.alias->n;
             for (uint64_t x = 0; x < cnt; ++x) {
@@ -1372,6 +1460,21 @@ int64_t fw2v_assemble_batch(const uint64_t* counts, int32_t vocab_size, const ui
         for (int64_t q = 0; q <= kept; ++q) out_offsets[q] = off[static_cast<size_t>(q)];
     });
     return rc == FW2V_OK ? kept : -rc;
+}
+
+int fw2v_alias_draws(const uint64_t* counts, int32_t vocab_size, double power, uint64_t seed, uint64_t count,
+                     int32_t* out) {
+    return guarded([&] {
+        if (vocab_size < 1) fail(FW2V_ERR_EMPTY_VOCAB, "empty vocabulary");
+        AliasTable at;
+        at.build(counts, vocab_size, power);
+        Rng r = Rng::derive(seed, 0);
+        if (have_avx512()) {
+            alias_draws_avx512(r.state, at.e.data(), at.n, out, count);
+        } else {
+            for (uint64_t x = 0; x < count; ++x) out[x] = at.sample(r.next());
+        }
+    });
 }
 
 float fw2v_lr_at(uint64_t words_trained, uint64_t total, float alpha0) {

@@ -115,7 +115,11 @@ struct K1sSmem {
     static constexpr int kGroupFloats = GPAD + 2 * NC * STRIDE + (RING ? C * STRIDE : 0);
     static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
+#ifdef KB_REGBLOCKS  // experiment: occupancy target for the no-ring kernels
+    static constexpr int kRegBlocks = VEC >= 8 ? (RING ? 5 : KB_REGBLOCKS) : 3;
+#else
     static constexpr int kRegBlocks = VEC >= 8 ? (RING ? 5 : 6) : 3;
+#endif
     static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
 };
 

@@ -45,7 +45,7 @@ EXPORTED = [
     "fw2v_plan_run", "fw2v_plan_destroy", "fw2v_keep_probs", "fw2v_table_build",
     "fw2v_assemble_batch", "fw2v_lr_at", "fw2v_analytic_traffic", "fw2v_corpus_synth_zipf",
     "fw2v_corpus_view", "fw2v_corpus_free", "fw2v_write_embeddings", "fw2v_save_model",
-    "fw2v_nearest_neighbors", "fw2v_eval_analogy",
+    "fw2v_nearest_neighbors", "fw2v_eval_analogy", "fw2v_alias_draws",
 ]
 
 
@@ -239,6 +239,14 @@ def assemble_batch(counts, offsets, ids, cursor, max_sentences, negatives, power
     off = o_off[: n + 1].copy()
     w = int(off[-1])
     return cur.value, off, o_ids[:w].copy(), o_negs[: w * negatives].copy()
+
+
+def alias_draws(counts, power, seed, count):
+    counts = np.ascontiguousarray(counts, np.uint64)
+    out = np.zeros(max(count, 1), np.int32)
+    _check(lib().fw2v_alias_draws(_p(counts, C.c_uint64), len(counts), C.c_double(power), C.c_uint64(seed),
+                                  C.c_uint64(count), _p(out, C.c_int32)))
+    return out[:count]
 
 
 def lr_at(trained, total, alpha0):

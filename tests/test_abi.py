@@ -119,3 +119,36 @@ def test_training_fails_loudly_without_device():
     with pytest.raises(fw.Fw2vError) as e:
         fw.Trainer(fw.TrainConfig(dim=16), counts)
     assert e.value.code == fw.fw2v.ERR_NO_DEVICE
+
+
+def test_alias_sampler_vector_and_scalar_paths_agree():
+    """The AVX-512 batching kernels (alias draws, subsampling) produce exactly
+    the scalar sequence: the same draws from the run with FW2V_NO_AVX512 set."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, paper_2312_07743_b200 as fw;"
+            "c=(np.arange(5000,0,-1)**1.5).astype(np.uint64);"
+            "print(fw.fw2v.alias_draws(c,0.75,7,100003).astype(np.int64).tobytes().hex())")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"FW2V_NO_AVX512": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root,
+                           env={**os.environ, **env}, check=True)
+        outs.append(r.stdout.strip())
+    assert outs[0] == outs[1]
+
+
+def test_alias_sampler_distribution():
+    """Draw frequencies follow count^0.75 (chi-square over the top 200 words)."""
+    import numpy as np
+
+    c = (np.arange(5000, 0, -1) ** 1.5).astype(np.uint64)
+    d = fw.fw2v.alias_draws(c, 0.75, 3, 2_000_000)
+    p = c.astype(np.float64) ** 0.75
+    p /= p.sum()
+    obs = np.bincount(d, minlength=len(c))[:200]
+    exp = p[:200] * len(d)
+    chi2 = ((obs - exp) ** 2 / exp).sum()
+    assert chi2 < 300  # 199 dof: mean 199, sd ~20
