@@ -115,11 +115,9 @@ struct K1sSmem {
     static constexpr int kGroupFloats = GPAD + 2 * NC * STRIDE + (RING ? C * STRIDE : 0);
     static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
-#ifdef KB_REGBLOCKS  // experiment: occupancy target for the no-ring kernels
-    static constexpr int kRegBlocks = VEC >= 8 ? (RING ? 5 : KB_REGBLOCKS) : 3;
-#else
-    static constexpr int kRegBlocks = VEC >= 8 ? (RING ? 5 : 6) : 3;
-#endif
+    // Register budget (blocks per SM the compiler must fit): 168 registers at
+    // 8 columns per lane (6 x 64 threads without the ring), ~220 at 10-12 columns.
+    static constexpr int kRegBlocks = VEC < 8 ? 3 : VEC > 8 ? 4 : (RING ? 5 : 6);
     static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
 };
 
