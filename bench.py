@@ -182,7 +182,7 @@ def run_ours(args, world, rank, local, dist):
                          workers=args.chunks, streams=args.streams, batch_sentences=args.batch_sentences,
                          subsample=1e-4,
                          seed=1 + rank, deterministic=0, reuse_mode=args.reuse_mode, device=local,
-                         sampler=args.sampler, l1_refresh_log2=args.l1_refresh_log2)
+                         sampler=args.sampler, l1_refresh_log2=args.l1_refresh_log2, k1_lanes=args.k1_lanes)
     trainer = fw.Trainer(cfg, corpus.counts)
     model = None
     if dist is not None:
@@ -337,6 +337,7 @@ def main():
     ap.add_argument("--reuse-mode", default="window_snapshot")
     ap.add_argument("--sampler", default="alias", choices=["reference", "alias"])
     ap.add_argument("--l1-refresh-log2", type=int, default=5)
+    ap.add_argument("--k1-lanes", type=int, default=0, help="lanes per sentence (0 = auto)")
     ap.add_argument("--ref-sentences", type=int, default=4000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

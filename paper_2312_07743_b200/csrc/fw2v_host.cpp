@@ -47,9 +47,10 @@ cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf,
 cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st);
 // Hot-row replicas: average = false broadcasts syn1 rows 0..K-1 into them, true averages them back.
 cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st);
+// K1s family: window-snapshot order, or (lifetime = true) the reference's lifetime order as a wavefront.
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
-                       DevCounters* ctr, cudaStream_t st, int* resident = nullptr);
-bool k1s_supported(int lanes, int vec, int n_neg, int wf);
+                       bool lifetime, DevCounters* ctr, cudaStream_t st, int* resident = nullptr);
+bool k1s_supported(int lanes, int vec, int n_neg, int wf, bool lifetime);
 int write_embeddings(const float* rows, int32_t vocab_size, int32_t dim, int64_t row_stride, const char* tokens,
                      const uint64_t* token_offsets, const char* path, int32_t threads, std::string* err);
 void set_last_error(const std::string& msg);
@@ -496,13 +497,13 @@ Shape choose_shape(int dim, int lanes_pref) {
 // sentences per warp amortise the per-window butterfly, sigmoid and
 // bookkeeping) with at most 8 columns per lane when the stride allows it
 // (registers), up to 12 on 32 lanes for wide rows (d = 300 -> 32 x 10).
-Shape choose_k1s_shape(int stride, const Shape& k1, int lanes_pref, int n_neg, int wf) {
+Shape choose_k1s_shape(int stride, const Shape& k1, int lanes_pref, int n_neg, int wf, bool lifetime) {
     if (lanes_pref == 0) {
         static const Shape pref[] = {{4, 4}, {8, 4}, {16, 4}, {16, 8}, {32, 4}, {32, 6}, {32, 8}, {32, 10}, {32, 12}};
         for (const Shape& s : pref)
-            if (s.lanes * s.vec == stride && k1s_supported(s.lanes, s.vec, n_neg, wf)) return s;
+            if (s.lanes * s.vec == stride && k1s_supported(s.lanes, s.vec, n_neg, wf, lifetime)) return s;
     }
-    return k1s_supported(k1.lanes, k1.vec, n_neg, wf) ? k1 : Shape{};
+    return k1s_supported(k1.lanes, k1.vec, n_neg, wf, lifetime) ? k1 : Shape{};
 }
 
 int row_stride_for(int dim, int lanes_pref) {
@@ -678,10 +679,13 @@ struct fw2v_ctx {
                            int* resident = nullptr) const {
         const ModelView mv = model_view();
         const bool fast = cfg.fast_sigmoid != 0;
+        // Lifetime order: the K1s wavefront where it applies (N <= 5), else K1.
+        if (!serial && cfg.reuse_mode == kLifetime && k1s_shape.lanes > 0)
+            return launch_k1s(k1s_shape.lanes, k1s_shape.vec, mv, bv, cfg.negatives, wf, fast, true, ctr, st, resident);
         if (!serial && cfg.reuse_mode == kLifetime && shape.lanes > 0 && wf <= 5)
             return launch_k1(shape.lanes, shape.vec, mv, bv, cfg.negatives, wf, fast, ctr, st, resident);
         if (!serial && cfg.reuse_mode == kWindowSnapshot && k1s_shape.lanes > 0)
-            return launch_k1s(k1s_shape.lanes, k1s_shape.vec, mv, bv, cfg.negatives, wf, fast, ctr, st, resident);
+            return launch_k1s(k1s_shape.lanes, k1s_shape.vec, mv, bv, cfg.negatives, wf, fast, false, ctr, st, resident);
         if (resident != nullptr) {
             *resident = 0;
             return cudaSuccess;
@@ -872,7 +876,10 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         x->deterministic = cfg->deterministic == 1 || (cfg->deterministic < 0 && x->cfg.workers == 1);
         x->shape = choose_shape(cfg->dim, cfg->k1_lanes);
         x->stride = row_stride_for(cfg->dim, cfg->k1_lanes);
-        x->k1s_shape = choose_k1s_shape(x->stride, x->shape, cfg->k1_lanes, cfg->negatives, x->wf);
+        x->k1s_shape = (cfg->reuse_mode == kWindowSnapshot || cfg->reuse_mode == kLifetime)
+                           ? choose_k1s_shape(x->stride, x->shape, cfg->k1_lanes, cfg->negatives, x->wf,
+                                              cfg->reuse_mode == kLifetime)
+                           : Shape{};
         if (!x->deterministic && cfg->reuse_mode == kLifetime && (x->shape.lanes == 0 || x->wf > 5))
             fail(FW2V_ERR_UNSUPPORTED, "K1 covers dim <= 512 and window <= 10 (W_f <= 5)");
         if (x->wf > 16) fail(FW2V_ERR_UNSUPPORTED, "window > 32 is not supported");
@@ -890,7 +897,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         Rng r = Rng::derive(cfg->seed, 0x696e6974ULL);  // "init" stream, model.cpp:26
         FW2V_CK(launch_init_model(x->model_view(), r.state, nullptr));
         FW2V_CK(cudaDeviceSynchronize());
-        if (!x->deterministic && cfg->reuse_mode == kWindowSnapshot && x->k1s_shape.lanes > 0 && cfg->hot_rows > 0) {
+        if (!x->deterministic && x->k1s_shape.lanes > 0 && cfg->hot_rows > 0) {
             x->hot_k = std::min(cfg->hot_rows, vocab_size);
             x->hot_r = cfg->hot_replicas;
             FW2V_CK(cudaMalloc(&x->hot_alloc, sizeof(float) * (static_cast<size_t>(x->hot_k) * x->hot_r + 1) * x->stride));

@@ -7,24 +7,25 @@ namespace fw2v {
 #define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(16, 8) X(32, 4) X(32, 6) X(32, 8) X(32, 10) X(32, 12)
 
 #define FW2V_EXTERN(L_, V_)                                                                                 \
-    extern template cudaError_t launch_k1s_shape<L_, V_>(const ModelView&, const BatchView&, int, int, bool, \
+    extern template cudaError_t launch_k1s_shape<L_, V_>(const ModelView&, const BatchView&, int, int, bool, bool, \
                                                          DevCounters*, cudaStream_t, int*);
 FW2V_K1S_SHAPES(FW2V_EXTERN)
 #undef FW2V_EXTERN
 
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
-                       DevCounters* ctr, cudaStream_t st, int* resident) {
+                       bool lifetime, DevCounters* ctr, cudaStream_t st, int* resident) {
 #define FW2V_CASE(L_, V_) \
-    if (lanes == L_ && vec == V_) return launch_k1s_shape<L_, V_>(m, b, n_neg, wf, fast, ctr, st, resident);
+    if (lanes == L_ && vec == V_) return launch_k1s_shape<L_, V_>(m, b, n_neg, wf, fast, lifetime, ctr, st, resident);
     FW2V_K1S_SHAPES(FW2V_CASE)
 #undef FW2V_CASE
     return cudaErrorInvalidValue;
 }
 
-// Any N: N + 1 <= 6 samples run as one chunk with the negatives in registers,
-// more as chunks of 4 or 6 loaded per window.
-bool k1s_supported(int lanes, int vec, int n_neg, int wf) {
-    if (n_neg < 0 || wf < 1 || wf > 5) return false;
+// Window-snapshot order: any N (N + 1 <= 6 samples run as one chunk with the
+// negatives in registers, more as chunks of 4 or 6 loaded per window).
+// Lifetime order (wavefront): N <= 5.
+bool k1s_supported(int lanes, int vec, int n_neg, int wf, bool lifetime) {
+    if (n_neg < 0 || wf < 1 || wf > 5 || (lifetime && n_neg > 5)) return false;
 #define FW2V_CASE(L_, V_) if (lanes == L_ && vec == V_) return true;
     FW2V_K1S_SHAPES(FW2V_CASE)
 #undef FW2V_CASE

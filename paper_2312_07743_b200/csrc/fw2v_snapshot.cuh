@@ -97,7 +97,7 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 constexpr int kPrefetchWindows = 16;
 
-template <int LANES, int VEC, int WF, int NC, bool RING = true>
+template <int LANES, int VEC, int WF, int NC, bool RING = true, bool LIFETIME = false>
 struct K1sSmem {
     static constexpr int NCTX = 2 * WF;
     static constexpr int C = 2 * WF + 1;
@@ -117,7 +117,12 @@ struct K1sSmem {
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
     // Register budget (blocks per SM the compiler must fit): 168 registers at
     // 8 columns per lane (6 x 64 threads without the ring), ~220 at 10-12 columns.
-    static constexpr int kRegBlocks = VEC < 8 ? 3 : VEC > 8 ? 4 : (RING ? 5 : 6);
+    // The register file is split between the 4 SMSPs (16K each): 5-6 blocks of
+    // 2 warps put 3 warps on some SMSP, 170 registers; 4 blocks allow 255.
+    // The lifetime wavefront keeps the window's sample rows in registers too.
+    // (measured at d=128: 4 blocks / 255 registers 661 M words/s, 6 blocks with
+    // spills 413).
+    static constexpr int kRegBlocks = VEC < 8 ? 3 : VEC > 8 || LIFETIME ? 4 : (RING ? 5 : 6);
     static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
 };
 
@@ -242,14 +247,23 @@ constexpr int kFullChunk = 0, kPartChunk = 1, kMultiChunk = 2;
 // write-back, or the finish() stash for the exact overwrite order). Without it
 // rows leaving the ring are stored straight back (Hogwild overwrite, the
 // reference's memcpy write-back, trainer.cpp:61-63, in any finish order).
-template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true>
-__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC, RING>::THREADS, K1sSmem<LANES, VEC, WF, NC, RING>::MINB)
+// LIFETIME: the reference's default update order instead (sweep_samples,
+// trainer.cpp:133-154: samples outer, contexts inner, every pairing sees the
+// previous pairings' updates). Pairing (k, j) depends only on (k, j-1) and
+// (k-1, j), so the 6 x 2W_f pairings of a window run as 2W_f + 5 anti-diagonal
+// steps of up to 6 independent dots (the wavefront), with the sample rows in
+// registers; windows whose sample ids repeat run the samples serially with the
+// rewritten row forwarded (the reference re-reads it, trainer.cpp:143).
+template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true, bool LIFETIME = false>
+__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>::THREADS,
+                                  K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>::MINB)
 k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ ctr) {
     static_assert(VEC % 2 == 0, "K1s stages 8- or 16-byte chunks");
+    static_assert(!LIFETIME || MODE != kMultiChunk, "lifetime order keeps all samples of a window in registers");
     constexpr bool MULTI = MODE == kMultiChunk;
     constexpr bool FULL = MODE == kFullChunk;
     const int n_neg = FULL ? NC - 1 : n_neg_arg;  // compile-time on the full-chunk path
-    using SM = K1sSmem<LANES, VEC, WF, NC, RING>;
+    using SM = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>;
     constexpr int NCTX = SM::NCTX;
     constexpr int C = SM::C;
     constexpr int NV = SM::NV;
@@ -404,6 +418,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
         // Next window's sample rows first (their buffer was last read in window
         // i-1); one cp.async group per window, so the wait below can leave it in flight.
         unsigned stale = 0;
+        bool dup = false;  // lifetime order: a sample id repeats inside the window
         if constexpr (!MULTI) {
             if (i + 1 < Lmax) prefetch(tok[WF], nnext, i + 1 < L && L >= 2, (i + 1) & 1);
             cp_async_commit();
@@ -420,6 +435,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 const unsigned upper = ((1u << HALF) - 1u) << (grp * LANES + HALF);
                 const bool st = sub < HALF && (mm & upper) != 0u;
                 stale = (__ballot_sync(kFull, st) >> (grp * LANES)) & ((1u << NC) - 1u);
+                if constexpr (LIFETIME) {
+                    const unsigned lower = ((1u << HALF) - 1u) << (grp * LANES);
+                    dup = __any_sync(kFull, sub < HALF && __popc(mm & lower) > 1);
+                }
                 prev_v = cv;
             } else {
                 int sq[NC];
@@ -434,6 +453,13 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 }
 #pragma unroll
                 for (int q = 0; q < NC; ++q) psid[q] = sq[q] >= 0 ? sq[q] : -100;
+                if constexpr (LIFETIME) {
+#pragma unroll
+                    for (int q = 1; q < NC; ++q)
+#pragma unroll
+                        for (int j = 0; j < q; ++j) dup |= sq[q] == sq[j];
+                    dup = __any_sync(kFull, dup);
+                }
             }
         }
         const int inc_tok = tok_ahead;
@@ -498,6 +524,79 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 }
             }
 
+            if constexpr (LIFETIME) {
+                // Sample rows of the window in registers (staged values = entry values).
+                float2 S[NC][H2];
+#pragma unroll
+                for (int q = 0; q < NC; ++q) SL::load_shared(S[q], cur + q * STRIDE);
+                auto pair_g = [&](int k, int j, float f) {
+                    const bool valid = wact && (FULL || k <= n_neg) && ((vmask >> j) & 1u) != 0u;
+                    return valid ? sgd_coeff<FAST>(f, k == 0 ? 1.0f : 0.0f, alpha) : 0.0f;
+                };
+                auto update = [&](int k, int j, float g) {  // pairing_update (kernels.hpp:26-33)
+                    const float2 gg = make_float2(g, g);
+#pragma unroll
+                    for (int h = 0; h < H2; ++h) {
+                        const float2 c = ctx[j][h];
+                        ctx[j][h] = __ffma2_rn(gg, S[k][h], c);
+                        S[k][h] = __ffma2_rn(gg, c, S[k][h]);
+                    }
+                };
+                auto dot = [&](int k, int j) {
+                    float2 acc = __fmul2_rn(ctx[j][0], S[k][0]);
+#pragma unroll
+                    for (int h = 1; h < H2; ++h) acc = __ffma2_rn(ctx[j][h], S[k][h], acc);
+                    return acc.x + acc.y;
+                };
+                if (!dup) {
+                    // Anti-diagonal d: pairings (k, d-k), independent of each other.
+#pragma unroll
+                    for (int d = 0; d < NC + NCTX - 1; ++d) {
+                        float f[NC];
+#pragma unroll
+                        for (int k = 0; k < NC; ++k)
+                            if (d - k >= 0 && d - k < NCTX) f[k] = dot(k, d - k);
+#pragma unroll
+                        for (int o = LANES / 2; o > 0; o >>= 1)
+#pragma unroll
+                            for (int k = 0; k < NC; ++k)
+                                if (d - k >= 0 && d - k < NCTX) f[k] += __shfl_xor_sync(kFull, f[k], o);
+#pragma unroll
+                        for (int k = 0; k < NC; ++k)
+                            if (d - k >= 0 && d - k < NCTX) update(k, d - k, pair_g(k, d - k, f[k]));
+                    }
+                } else {
+                    // Reference order, sample by sample; a repeated id starts from the
+                    // row its previous occurrence left (the reference re-reads it).
+#pragma unroll
+                    for (int k = 0; k < NC; ++k) {
+#pragma unroll
+                        for (int k2 = 0; k2 < k; ++k2)
+                            if (sid[k2] == sid[k]) vcopy2(S[k], S[k2]);
+#pragma unroll
+                        for (int j = 0; j < NCTX; ++j) {
+                            float f = dot(k, j);
+#pragma unroll
+                            for (int o = LANES / 2; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
+                            update(k, j, pair_g(k, j, f));
+                        }
+                    }
+                }
+                // Sample write-back: one row += (final - staged) per distinct id, at its
+                // last occurrence (earlier occurrences were forwarded into it).
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    bool last_occ = true;
+#pragma unroll
+                    for (int q2 = q + 1; q2 < NC; ++q2) last_occ &= sid[q2] != sid[q];
+                    float2 e[H2];
+                    SL::load_shared(e, cur + q * STRIDE);
+#pragma unroll
+                    for (int h = 0; h < H2; ++h) e[h] = make_float2(S[q][h].x - e[h].x, S[q][h].y - e[h].y);
+                    if constexpr (FULL) SL::red_add_if(wact && (last_occ || !dup), srow(sid[q]), e);
+                    else SL::red_add_if(sid[q] >= 0 && (last_occ || !dup), srow(max(sid[q], 0)), e);
+                }
+            } else {
             KB_T(2)
             // 1-2. all dots of the chunk (window-entry values), one transposed butterfly.
             float P[NV];
@@ -580,6 +679,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                     }
                 }
             }
+            }  // snapshot
             if constexpr (MULTI) __syncwarp();  // the next chunk rewrites sbuf
         }
         if constexpr (MULTI) {
@@ -696,12 +796,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
 }
 
 // ------------------------------------------------------------------ dispatch
-template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true>
+template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING, bool LIFETIME>
 cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, int n_neg, DevCounters* ctr,
                             cudaStream_t st, int* resident) {
-    using SMx = K1sSmem<LANES, VEC, WF, NC, RING>;
+    using SMx = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>;
     constexpr int bytes = SMx::kBlockBytes;
-    auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MODE, FAST, RING>;
+    auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MODE, FAST, RING, LIFETIME>;
     static bool configured = false;  // benign race: idempotent attribute set
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -715,38 +815,46 @@ cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, 
     return cudaGetLastError();
 }
 
+// Sigmoid and ring variants of one mode; the Hogwild overwrite (no shared-memory
+// ring) is built for the fast sigmoid only.
+template <int LANES, int VEC, int WF, int NC, int MODE, bool LIFETIME>
+cudaError_t launch_k1s_mode(int blocks, const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
+                            cudaStream_t st, int* resident) {
+    if (fast && (m.flags & kFlagNoRing) != 0)
+        return launch_k1s_inst<LANES, VEC, WF, NC, MODE, true, false, LIFETIME>(blocks, m, b, n_neg, ctr, st, resident);
+    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, MODE, true, true, LIFETIME>(blocks, m, b, n_neg, ctr, st, resident)
+                : launch_k1s_inst<LANES, VEC, WF, NC, MODE, false, true, LIFETIME>(blocks, m, b, n_neg, ctr, st, resident);
+}
+
 template <int LANES, int VEC, int WF, int NC>
-cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
-                          cudaStream_t st, int* resident) {
+cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, bool lifetime,
+                          DevCounters* ctr, cudaStream_t st, int* resident) {
     constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;  // RING does not change THREADS
     const int blocks = (b.n_sentences + per_block - 1) / per_block;
-    if (n_neg + 1 > NC)
-        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true>(blocks, m, b, n_neg, ctr, st, resident)
-                    : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false>(blocks, m, b, n_neg, ctr, st, resident);
-    // Hogwild overwrite (no shared-memory ring) is built for the fast sigmoid only.
-    const bool no_ring = fast && (m.flags & kFlagNoRing) != 0;
-    if (n_neg + 1 < NC) {
-        if (no_ring) return launch_k1s_inst<LANES, VEC, WF, NC, kPartChunk, true, false>(blocks, m, b, n_neg, ctr, st, resident);
-        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kPartChunk, true>(blocks, m, b, n_neg, ctr, st, resident)
-                    : launch_k1s_inst<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, ctr, st, resident);
+    if (n_neg + 1 > NC) {
+        if (lifetime) return cudaErrorInvalidValue;  // the lifetime order keeps <= NC samples in registers
+        return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, false>(blocks, m, b, n_neg, ctr, st, resident)
+                    : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, false>(blocks, m, b, n_neg, ctr, st, resident);
     }
-    if (no_ring) return launch_k1s_inst<LANES, VEC, WF, NC, kFullChunk, true, false>(blocks, m, b, n_neg, ctr, st, resident);
-    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, ctr, st, resident)
-                : launch_k1s_inst<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, ctr, st, resident);
+    if (n_neg + 1 < NC)
+        return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
+                        : launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+    return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
+                    : launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
 }
 
 template <int LANES, int VEC>
-cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
+cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast, bool lifetime,
                              DevCounters* ctr, cudaStream_t st, int* resident) {
     switch (wf) {
-    case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, ctr, st, resident);
-    case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, ctr, st, resident);
-    case 3: return launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, ctr, st, resident);
+    case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
+    case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
+    case 3: return launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
     // Wide windows: one 6-sample chunk when N+1 <= 6, else 4-sample chunks (registers).
-    case 4: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 4, 6>(m, b, n_neg, fast, ctr, st, resident)
-                                  : launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, ctr, st, resident);
-    case 5: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 5, 6>(m, b, n_neg, fast, ctr, st, resident)
-                                  : launch_k1s_nc<LANES, VEC, 5, 4>(m, b, n_neg, fast, ctr, st, resident);
+    case 4: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 4, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident)
+                                  : launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, lifetime, ctr, st, resident);
+    case 5: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 5, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident)
+                                  : launch_k1s_nc<LANES, VEC, 5, 4>(m, b, n_neg, fast, lifetime, ctr, st, resident);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -3,6 +3,6 @@
 #include "fw2v_snapshot.cuh"
 
 namespace fw2v {
-template cudaError_t launch_k1s_shape<32, 10>(const ModelView&, const BatchView&, int, int, bool, DevCounters*,
-                                               cudaStream_t, int*);
+template cudaError_t launch_k1s_shape<32, 10>(const ModelView&, const BatchView&, int, int, bool, bool,
+                                               DevCounters*, cudaStream_t, int*);
 } // namespace fw2v

@@ -126,7 +126,7 @@ def test_k1_distinct_tokens_batch_equals_serial(oracle):
     ro = (ri[::-1] * 4.0).copy()
     gi0, go0 = ri.copy(), ro.copy()
     oracle.train_sentences(ri, ro, offsets, ids, np.zeros(0, np.int32), alphas, OConfig(**cfg))
-    with _trainer(counts=counts, deterministic=0, fast_sigmoid=False, **cfg) as t:
+    with _trainer(counts=counts, deterministic=0, fast_sigmoid=False, hot_rows=0, **cfg) as t:
         t.set_model(gi0, go0)
         t.train_sentences(offsets, ids, np.zeros(0, np.int32), alphas, serial=False)
         gi, go = t.get_model()

@@ -20,6 +20,9 @@
 #ifndef KB_RING
 #define KB_RING true
 #endif
+#ifndef KB_LIFE
+#define KB_LIFE false
+#endif
 #ifndef KB_PAD
 #define KB_PAD 0
 #endif
@@ -93,10 +96,10 @@ int main(int argc, char** argv) {
         for (int c = 0; c < chunks; ++c) {
             const int64_t s0 = kept * c / chunks, s1 = kept * (c + 1) / chunks;
             fw2v::BatchView b{dids, doff + s0, dnegs, dalpha + s0, static_cast<int32_t>(s1 - s0)};
-            using SMx = fw2v::K1sSmem<KB_LANES, KB_VEC, 3, 6, KB_RING>;
+            using SMx = fw2v::K1sSmem<KB_LANES, KB_VEC, 3, 6, KB_RING, KB_LIFE>;
             const int per_block = SMx::THREADS / KB_LANES;
             const int blocks = static_cast<int>((s1 - s0 + per_block - 1) / per_block);
-            auto* kern = fw2v::k1s_snapshot<KB_LANES, KB_VEC, 3, 6, fw2v::kFullChunk, true, KB_RING>;
+            auto* kern = fw2v::k1s_snapshot<KB_LANES, KB_VEC, 3, 6, fw2v::kFullChunk, true, KB_RING, KB_LIFE>;
             const int bytes = SMx::kBlockBytes + KB_PAD;
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
             kern<<<blocks, SMx::THREADS, bytes, ss[c]>>>(m, b, N, dctr);
@@ -134,9 +137,9 @@ int main(int argc, char** argv) {
     float mx0 = 0; for (float v : in0) if (std::isfinite(v)) mx0 = std::max(mx0, std::fabs(v)); else ++bad;
     printf("max|syn1| %.4g max|syn0| %.4g nonfinite %zu  ", mx, mx0, bad);
     {
-        using SMx = fw2v::K1sSmem<KB_LANES, KB_VEC, 3, 6, KB_RING>;
+        using SMx = fw2v::K1sSmem<KB_LANES, KB_VEC, 3, 6, KB_RING, KB_LIFE>;
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fw2v::k1s_snapshot<KB_LANES, KB_VEC, 3, 6, fw2v::kFullChunk, true, KB_RING>,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fw2v::k1s_snapshot<KB_LANES, KB_VEC, 3, 6, fw2v::kFullChunk, true, KB_RING, KB_LIFE>,
                                                          SMx::THREADS, SMx::kBlockBytes + KB_PAD));
         printf("[%d blocks/SM x %d threads] ", per_sm, SMx::THREADS);
     }
