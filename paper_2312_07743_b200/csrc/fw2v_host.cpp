@@ -552,12 +552,14 @@ struct Slot {
     uint32_t* d_off = nullptr;
     int32_t* d_negs = nullptr;
     float* d_alpha = nullptr;
-    cudaEvent_t h2d_done = nullptr;
+    cudaEvent_t h2d_done = nullptr;  // host buffers free again (copy stream)
+    cudaEvent_t used = nullptr;      // device buffers free again (kernel done, compute stream)
     bool in_flight = false;
 };
 
 struct Lane {
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;  // kernels
+    cudaStream_t copy = nullptr;    // H2D of the next sub-batch, overlapping the current kernel
     DevCounters* d_ctr = nullptr;
     Slot slot[2];
     uint64_t cap_words = 0, cap_sent = 0;
@@ -567,6 +569,7 @@ struct Lane {
             cudaFreeHost(s.h_ids); cudaFreeHost(s.h_off); cudaFreeHost(s.h_negs); cudaFreeHost(s.h_alpha);
             cudaFree(s.d_ids); cudaFree(s.d_off); cudaFree(s.d_negs); cudaFree(s.d_alpha);
             if (s.h2d_done) cudaEventDestroy(s.h2d_done);
+            if (s.used) cudaEventDestroy(s.used);
             s = Slot{};
         }
         cap_words = cap_sent = 0;
@@ -700,6 +703,7 @@ struct fw2v_ctx {
         for (int i = 0; i < n; ++i) {
             Lane& ln = lanes[static_cast<size_t>(i)];
             if (!ln.stream) FW2V_CK(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+            if (!ln.copy) FW2V_CK(cudaStreamCreateWithFlags(&ln.copy, cudaStreamNonBlocking));
             if (!ln.d_ctr) FW2V_CK(cudaMalloc(&ln.d_ctr, sizeof(DevCounters)));
             if (ln.cap_words >= cap_words && ln.cap_sent >= cap_sent) continue;
             ln.release();
@@ -713,6 +717,7 @@ struct fw2v_ctx {
                 FW2V_CK(cudaMalloc(&s.d_off, 4 * (cap_sent + 1)));
                 FW2V_CK(cudaMalloc(&s.d_alpha, 4 * cap_sent));
                 FW2V_CK(cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming));
+                FW2V_CK(cudaEventCreateWithFlags(&s.used, cudaEventDisableTiming));
             }
             ln.cap_words = cap_words;
             ln.cap_sent = cap_sent;
@@ -723,9 +728,11 @@ struct fw2v_ctx {
         cudaSetDevice(cfg.device);
         for (Lane& ln : lanes) {
             if (ln.stream) cudaStreamSynchronize(ln.stream);
+            if (ln.copy) cudaStreamSynchronize(ln.copy);
             ln.release();
             cudaFree(ln.d_ctr);
             if (ln.stream) cudaStreamDestroy(ln.stream);
+            if (ln.copy) cudaStreamDestroy(ln.copy);
         }
         cudaFree(hot_alloc);
         if (own_model) {
@@ -1172,12 +1179,16 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                                 for (uint64_t q = 0; q < kept; ++q)
                                     for (uint32_t i = 0; i < sl.h_off[q + 1] - sl.h_off[q]; ++i) observer(observer_user, s0 + q, i);
                             }
-                            cudaStream_t st = ln.stream;
-                            FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, st));
-                            if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, st));
-                            FW2V_CK(cudaMemcpyAsync(sl.d_off, sl.h_off, 4 * (kept + 1), cudaMemcpyHostToDevice, st));
-                            FW2V_CK(cudaMemcpyAsync(sl.d_alpha, sl.h_alpha, 4 * kept, cudaMemcpyHostToDevice, st));
-                            FW2V_CK(cudaEventRecord(sl.h2d_done, st));
+                            // H2D on the lane's copy stream once the kernel that last read
+                            // this slot's device buffers is done; the kernel waits for the copy.
+                            cudaStream_t st = ln.stream, cs = ln.copy;
+                            if (sl.in_flight) FW2V_CK(cudaStreamWaitEvent(cs, sl.used, 0));
+                            FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, cs));
+                            if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, cs));
+                            FW2V_CK(cudaMemcpyAsync(sl.d_off, sl.h_off, 4 * (kept + 1), cudaMemcpyHostToDevice, cs));
+                            FW2V_CK(cudaMemcpyAsync(sl.d_alpha, sl.h_alpha, 4 * kept, cudaMemcpyHostToDevice, cs));
+                            FW2V_CK(cudaEventRecord(sl.h2d_done, cs));
+                            FW2V_CK(cudaStreamWaitEvent(st, sl.h2d_done, 0));
                             sl.in_flight = true;
                             h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
                             const BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
@@ -1190,6 +1201,7 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                                 FW2V_CK(cudaEventRecord(rec.k0, st));
                             }
                             FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, P));
+                            FW2V_CK(cudaEventRecord(sl.used, st));
                             if (trace) {
                                 FW2V_CK(cudaEventRecord(rec.k1, st));
                                 rec.t2 = wall_seconds() - t0;
