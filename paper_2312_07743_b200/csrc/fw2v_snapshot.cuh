@@ -419,6 +419,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
         // i-1); one cp.async group per window, so the wait below can leave it in flight.
         unsigned stale = 0;
         bool dup = false;  // lifetime order: a sample id repeats inside the window
+        unsigned match_mask = 0;
         if constexpr (!MULTI) {
             if (i + 1 < Lmax) prefetch(tok[WF], nnext, i + 1 < L && L >= 2, (i + 1) & 1);
             cp_async_commit();
@@ -431,14 +432,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 for (int k = 0; k < NN; ++k) cv = q == k + 1 ? ncur[k] : cv;
                 cv = (wact && q <= n_neg && q < NC) ? cv : -1 - lane;
                 const int mv = sub < HALF ? cv : prev_v;
-                const unsigned mm = __match_any_sync(kFull, mv);
-                const unsigned upper = ((1u << HALF) - 1u) << (grp * LANES + HALF);
-                const bool st = sub < HALF && (mm & upper) != 0u;
-                stale = (__ballot_sync(kFull, st) >> (grp * LANES)) & ((1u << NC) - 1u);
-                if constexpr (LIFETIME) {
-                    const unsigned lower = ((1u << HALF) - 1u) << (grp * LANES);
-                    dup = __any_sync(kFull, sub < HALF && __popc(mm & lower) > 1);
-                }
+                match_mask = __match_any_sync(kFull, mv);  // consumed after the wait below
                 prev_v = cv;
             } else {
                 int sq[NC];
@@ -503,6 +497,15 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 // Rows staged by cp.async during the previous window; slots
                 // without a sample hold finite stale rows and get g = 0.
                 KB_T(0)
+                if constexpr (kMatch) {  // the match issued at the top of the window has landed
+                    const unsigned upper = ((1u << HALF) - 1u) << (grp * LANES + HALF);
+                    const bool st = sub < HALF && (match_mask & upper) != 0u;
+                    stale = (__ballot_sync(kFull, st) >> (grp * LANES)) & ((1u << NC) - 1u);
+                    if constexpr (LIFETIME) {
+                        const unsigned lower = ((1u << HALF) - 1u) << (grp * LANES);
+                        dup = __any_sync(kFull, sub < HALF && __popc(match_mask & lower) > 1);
+                    }
+                }
                 cp_async_wait_group<1>();
                 KB_T(1)
                 cur = sbuf + (i & 1) * NC * STRIDE;
@@ -561,6 +564,8 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
 #pragma unroll
                             for (int k = 0; k < NC; ++k)
                                 if (d - k >= 0 && d - k < NCTX) f[k] += __shfl_xor_sync(kFull, f[k], o);
+                        // (g evaluated by every lane: a lane-distributed sigmoid with
+                        // shuffled g measured 7% slower; the wavefront is latency-bound)
 #pragma unroll
                         for (int k = 0; k < NC; ++k)
                             if (d - k >= 0 && d - k < NCTX) update(k, d - k, pair_g(k, d - k, f[k]));
