@@ -303,7 +303,7 @@ def run_ours(args, world, rank, local, dist):
                          "bytes_per_word": bpw,
                          "note": "algorithmic lifetime-mode bytes/word x words/s; the model is L2-resident "
                                  "so frac can exceed 1"},
-            "e2e": e2e, "gpu_launches": n_launches * args.steps, "clocks": clocks,
+            "e2e": e2e, "gpu_launches": (n_launches + (2 if cfg.hot_rows > 0 else 0)) * args.steps, "clocks": clocks,
             "wall_s_timed": wall,
         }
         if cpu_baseline is not None:

@@ -97,7 +97,12 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 constexpr int kPrefetchWindows = 16;
 
-template <int LANES, int VEC, int WF, int NC, bool RING = true, bool LIFETIME = false>
+// Window-snapshot order with more than NC samples keeps every sample row of the
+// window in shared memory (read at window entry, before any of the window's
+// reductions): up to kMaxSnapSamples = N + 1.
+constexpr int kMaxSnapSamples = 16;
+
+template <int LANES, int VEC, int WF, int NC, bool RING = true, bool LIFETIME = false, bool SNAPALL = false>
 struct K1sSmem {
     static constexpr int NCTX = 2 * WF;
     static constexpr int C = 2 * WF + 1;
@@ -112,7 +117,8 @@ struct K1sSmem {
     // (delta write-back) or the finish() stash (overwrite) — never both.
     // RING = false (Hogwild overwrite write-back): ring rows leave straight to HBM,
     // no shared-memory ring: 64% of the footprint, 6 blocks per SM at d=128.
-    static constexpr int kGroupFloats = GPAD + 2 * NC * STRIDE + (RING ? C * STRIDE : 0);
+    static constexpr int SROWS = SNAPALL ? (kMaxSnapSamples > 2 * NC ? kMaxSnapSamples : 2 * NC) : 2 * NC;
+    static constexpr int kGroupFloats = GPAD + SROWS * STRIDE + (RING ? C * STRIDE : 0);
     static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
     // Register budget (blocks per SM the compiler must fit): 168 registers at
@@ -255,15 +261,14 @@ constexpr int kFullChunk = 0, kPartChunk = 1, kMultiChunk = 2;
 // registers; windows whose sample ids repeat run the samples serially with the
 // rewritten row forwarded (the reference re-reads it, trainer.cpp:143).
 template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true, bool LIFETIME = false>
-__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>::THREADS,
-                                  K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>::MINB)
+__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == 2 && !LIFETIME>::THREADS,
+                                  K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == 2 && !LIFETIME>::MINB)
 k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ ctr) {
     static_assert(VEC % 2 == 0, "K1s stages 8- or 16-byte chunks");
-    static_assert(!LIFETIME || MODE != kMultiChunk, "lifetime order keeps all samples of a window in registers");
     constexpr bool MULTI = MODE == kMultiChunk;
     constexpr bool FULL = MODE == kFullChunk;
     const int n_neg = FULL ? NC - 1 : n_neg_arg;  // compile-time on the full-chunk path
-    using SM = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>;
+    using SM = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == kMultiChunk && !LIFETIME>;
     constexpr int NCTX = SM::NCTX;
     constexpr int C = SM::C;
     constexpr int NV = SM::NV;
@@ -291,7 +296,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
     const bool has = sent < b.n_sentences;
     float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
     float* sbuf = gsh + SM::GPAD + sub * SL::CW;                  // + (parity*NC + q)*STRIDE
-    float* ring = gsh + SM::GPAD + 2 * NC * STRIDE + sub * SL::CW;  // + slot*STRIDE
+    float* ring = gsh + SM::GPAD + SM::SROWS * STRIDE + sub * SL::CW;  // + slot*STRIDE
     const bool delta_wb = RING && (m.flags & kFlagDeltaRing) != 0;
 
     uint32_t beg = 0, len = 0;
@@ -372,7 +377,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
 
     {
 #pragma unroll
-        for (int q = 0; q < 2 * NC; ++q)
+        for (int q = 0; q < SM::SROWS; ++q)
 #pragma unroll
             SL::zero_shared(sbuf + q * STRIDE);
     }
@@ -472,11 +477,21 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
             prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
         }
         c_reads += inc_tok >= 0;
-        if constexpr (MULTI) {
+        if constexpr (MULTI && !LIFETIME) {
 #pragma unroll
             for (int r = 0; r < NCTX; ++r) vzero2(dctx[r]);
         }
 
+        if constexpr (MULTI && !LIFETIME) {
+            // Snapshot order: every sample row of the window as it is before any of
+            // the window's reductions (sweep_samples_snapshot, trainer.cpp:158-205).
+            for (int kk = 0; kk <= n_neg; ++kk) {
+                const int s = kk == 0 ? ttok : (wact ? __ldg(negs + i * n_neg + kk - 1) : -1);
+                float2 v[H2];
+                SL::load(v, srow(max(s, 0)));
+                SL::store_shared(sbuf + kk * STRIDE, v);
+            }
+        }
         const int n_chunks = MULTI ? (n_neg + NC) / NC : 1;
         for (int ch = 0; ch < n_chunks; ++ch) {
             const int kbase = MULTI ? ch * NC : 0;
@@ -518,12 +533,24 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                             SL::store_shared(const_cast<float*>(cur) + q * STRIDE, v);
                         }
                 }
+            } else if constexpr (!LIFETIME) {
+                cur = sbuf + kbase * STRIDE;  // rows staged at window entry
             } else {
+                // Lifetime order: chunk rows read now include every reduction this
+                // thread issued before (earlier chunks of the window).
 #pragma unroll
                 for (int q = 0; q < NC; ++q) {
                     float2 v[H2];
                     SL::load(v, srow(max(sid[q], 0)));
                     SL::store_shared(sbuf + q * STRIDE, v);
+                }
+                {
+                    bool d = false;
+#pragma unroll
+                    for (int q = 1; q < NC; ++q)
+#pragma unroll
+                        for (int j = 0; j < q; ++j) d |= sid[q] >= 0 && sid[q] == sid[j];
+                    dup = __any_sync(kFull, d);
                 }
             }
 
@@ -533,8 +560,8 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
 #pragma unroll
                 for (int q = 0; q < NC; ++q) SL::load_shared(S[q], cur + q * STRIDE);
                 auto pair_g = [&](int k, int j, float f) {
-                    const bool valid = wact && (FULL || k <= n_neg) && ((vmask >> j) & 1u) != 0u;
-                    return valid ? sgd_coeff<FAST>(f, k == 0 ? 1.0f : 0.0f, alpha) : 0.0f;
+                    const bool valid = wact && (FULL || kbase + k <= n_neg) && ((vmask >> j) & 1u) != 0u;
+                    return valid ? sgd_coeff<FAST>(f, kbase + k == 0 ? 1.0f : 0.0f, alpha) : 0.0f;
                 };
                 auto update = [&](int k, int j, float g) {  // pairing_update (kernels.hpp:26-33)
                     const float2 gg = make_float2(g, g);
@@ -687,7 +714,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
             }  // snapshot
             if constexpr (MULTI) __syncwarp();  // the next chunk rewrites sbuf
         }
-        if constexpr (MULTI) {
+        if constexpr (MULTI && !LIFETIME) {
 #pragma unroll
             for (int r = 0; r < NCTX; ++r)
 #pragma unroll
@@ -804,7 +831,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
 template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING, bool LIFETIME>
 cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, int n_neg, DevCounters* ctr,
                             cudaStream_t st, int* resident) {
-    using SMx = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME>;
+    using SMx = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == kMultiChunk && !LIFETIME>;
     constexpr int bytes = SMx::kBlockBytes;
     auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MODE, FAST, RING, LIFETIME>;
     static bool configured = false;  // benign race: idempotent attribute set
@@ -837,15 +864,28 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
     constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;  // RING does not change THREADS
     const int blocks = (b.n_sentences + per_block - 1) / per_block;
     if (n_neg + 1 > NC) {
-        if (lifetime) return cudaErrorInvalidValue;  // the lifetime order keeps <= NC samples in registers
+        // Chunks of NC samples; in lifetime order each chunk is its own wavefront,
+        // started from the contexts the previous chunk left (exact order).
+        if constexpr (VEC <= 10) {
+            if (lifetime)
+                return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, true>(blocks, m, b, n_neg, ctr, st, resident)
+                            : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, true>(blocks, m, b, n_neg, ctr, st, resident);
+        }
+        if (lifetime) return cudaErrorInvalidValue;
         return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, false>(blocks, m, b, n_neg, ctr, st, resident)
                     : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, false>(blocks, m, b, n_neg, ctr, st, resident);
     }
-    if (n_neg + 1 < NC)
-        return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
-                        : launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
-    return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
-                    : launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+    if constexpr (VEC > 10) {  // lifetime order: the window's sample rows would not fit in registers
+        if (lifetime) return cudaErrorInvalidValue;
+        if (n_neg + 1 < NC) return launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+        return launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+    } else {
+        if (n_neg + 1 < NC)
+            return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
+                            : launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+        return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
+                        : launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+    }
 }
 
 template <int LANES, int VEC>

@@ -250,3 +250,36 @@ def test_k1s_overwrite_without_ring_matches_delta(dim):
             out[mode] = t.get_model()
     for a, b in zip(out[1], out[2]):
         assert np.abs(a - b).max() <= 1e-6 * np.abs(a).max() + 1e-8
+
+
+@pytest.mark.parametrize("mode", ["lifetime", "window_snapshot"])
+@pytest.mark.parametrize("dim,window,n_neg", [(128, 5, 0), (128, 5, 2), (128, 5, 15), (32, 5, 15), (128, 9, 15),
+                                              (64, 3, 9), (300, 5, 11), (512, 5, 5)])
+def test_k1s_negative_counts_single_sentence(oracle, mode, dim, window, n_neg):
+    """K1s with any number of negatives (partial chunk, several chunks per window;
+    lifetime order: one wavefront per chunk) == the reference order per sentence,
+    up to FP association; sentences with repeated ids included."""
+    counts, offsets, ids = random_corpus(4, 40, 20, seed=dim + 3 * n_neg + window, min_len=1)
+    V = len(counts)
+    negs = fixed_negatives(int(offsets[-1]), n_neg, V, seed=n_neg)
+    alphas = np.full(len(offsets) - 1, 0.025, np.float32)
+    cfg = dict(dim=dim, window=window, negatives=n_neg, workers=4, reuse_mode=mode)
+    gcfg = dict(cfg, deterministic=0, fast_sigmoid=False, l1_refresh_log2=0, delta_writeback=False, hot_rows=0)
+    ri, _ = oracle.init_model(V, dim, 5)
+    ro = (ri[::-1] * 4.0).copy()
+    gi0, go0 = ri.copy(), ro.copy()
+    for s in range(len(offsets) - 1):
+        o = offsets[s:s + 2] - offsets[s]
+        sl = ids[int(offsets[s]):int(offsets[s + 1])]
+        ng = negs[int(offsets[s]) * n_neg:int(offsets[s + 1]) * n_neg]
+        oracle.train_sentences(ri, ro, o, sl, ng, alphas[s:s + 1], OConfig(**cfg))
+    with _trainer(counts=counts, **gcfg) as t:
+        t.set_model(gi0, go0)
+        for s in range(len(offsets) - 1):
+            o = offsets[s:s + 2] - offsets[s]
+            sl = ids[int(offsets[s]):int(offsets[s + 1])]
+            ng = negs[int(offsets[s]) * n_neg:int(offsets[s + 1]) * n_neg]
+            t.train_sentences(o, sl, ng, alphas[s:s + 1], serial=False)
+        gi, go = t.get_model()
+    assert np.abs(gi - ri).max() <= 2e-5 * np.abs(ri).max() + 1e-7
+    assert np.abs(go - ro).max() <= 2e-5 * np.abs(ro).max() + 1e-7
