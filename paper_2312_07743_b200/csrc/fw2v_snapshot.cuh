@@ -559,9 +559,16 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 float2 S[NC][H2];
 #pragma unroll
                 for (int q = 0; q < NC; ++q) SL::load_shared(S[q], cur + q * STRIDE);
+                // Per-window constants: context validity (this window, as a mask of
+                // the active slots) and the folded fast-sigmoid coefficients.
+                const unsigned vm = wact ? vmask : 0u;
+                const float al1 = 0.5f * alpha, al0 = -0.5f * alpha, nha = -0.5f * alpha;
                 auto pair_g = [&](int k, int j, float f) {
-                    const bool valid = wact && (FULL || kbase + k <= n_neg) && ((vmask >> j) & 1u) != 0u;
-                    return valid ? sgd_coeff<FAST>(f, kbase + k == 0 ? 1.0f : 0.0f, alpha) : 0.0f;
+                    const bool valid = ((vm >> j) & 1u) != 0u && (FULL || kbase + k <= n_neg);
+                    float g;
+                    if constexpr (FAST) g = sgd_coeff_fast(f, kbase + k == 0 ? al1 : al0, nha);
+                    else g = sgd_coeff<FAST>(f, kbase + k == 0 ? 1.0f : 0.0f, alpha);
+                    return valid ? g : 0.0f;
                 };
                 auto update = [&](int k, int j, float g) {  // pairing_update (kernels.hpp:26-33)
                     const float2 gg = make_float2(g, g);
@@ -668,7 +675,10 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                     valid = wact && ((w >> 16) & 1u) && vbit;
                     label = ((w >> 17) & 1u) ? 1.0f : 0.0f;
                 }
-                gsh[w & 255u] = valid ? sgd_coeff<FAST>(P[j], label, alpha) : 0.0f;
+                float g;
+                if constexpr (FAST) g = sgd_coeff_fast(P[j], alpha * (label - 0.5f), -0.5f * alpha);
+                else g = sgd_coeff<FAST>(P[j], label, alpha);
+                gsh[w & 255u] = valid ? g : 0.0f;
             }
             __syncwarp();
             float g[SM::GPAD];
