@@ -40,7 +40,8 @@ struct ModelView {
 };
 
 // K1s memory-path options.
-constexpr int32_t kFlagRedSamples = 1;    // sample rows: red.global.add of the delta (no lost updates)
+constexpr int32_t kFlagRedSamples = 1;    // sample rows are written as red.global.add of the delta (always set;
+                                          // documents the write-back in flag dumps)
 constexpr int32_t kFlagL1Exact = 2;       // K1s sample rows are staged through L1 (cp.async.ca); every warp
                                           // drops its SM's L1 each window, so reads see the sentence's own writes
 constexpr int32_t kFlagDeltaRing = 4;     // ring rows written back as red.add(final - loaded)

@@ -1,26 +1,28 @@
-// K1s — FULL-W2V window kernel with independent negatives (the paper's update
-// rule; reference oracle: sweep_samples_snapshot,
-// trainer.cpp:158-205, ReuseMode::window_snapshot).
+// K1s — the FULL-W2V window kernels for B200 (sm_100a, CUDA cores).
 //
-// Every (sample, context) pairing of a window is computed from window-entry
-// values, so the (N+1) x 2W_f dots of a window are independent:
-//   1. the N+1 sample rows (syn1) of window i+1 are prefetched with cp.async
-//      (16 B per lane, L2 only) into shared memory while window i computes;
-//   2. all dots are formed per lane on VEC columns with packed FFMA2
-//      (sm_100 fma.rn.f32x2) and reduced across the LANES lanes of the
-//      sentence's group with ONE transposed butterfly: at each xor level a lane
-//      keeps half of its partial sums and sends the other half, so NV dots cost
-//      ~NV shuffles in total instead of NV*log2(LANES);
-//   3. each lane evaluates the sigmoid for the dots it ended up owning and
-//      publishes g as (g, g) pairs in shared memory;
-//   4. sample deltas D_k = sum_r g_kr c_r and context updates
-//      c_r += sum_k g_kr s_k are FFMA2 on registers; samples are written once
-//      per window (row += delta, trainer.cpp:198-204).
+// Window-snapshot order (the paper's independent-negatives rule, PAPER.md:519-529;
+// reference oracle sweep_samples_snapshot, trainer.cpp:158-205): every (sample,
+// context) pairing of a window uses window-entry values, so the (N+1) x 2W_f dots
+// are independent:
+//   1. window i+1's N+1 sample rows (syn1) are staged by cp.async (through L1)
+//      into shared memory while window i computes; rows the previous window
+//      rewrote after their prefetch are found with one __match_any_sync and re-read;
+//   2. all dots are formed per lane on its column slice with packed FFMA2
+//      (fma.rn.f32x2) and reduced across the sentence's lane group by ONE
+//      transposed butterfly (each level keeps half of the partial sums and ships
+//      the other half: ~1 shuffle per dot); the top level is select-free because
+//      lanes of the upper half read the sample rows in swapped order;
+//   3. each lane evaluates the sigmoid of the dots it owns; g goes through shared
+//      memory to the whole group;
+//   4. sample deltas D_k = sum_r g_kr c_r (written as red.global.add, row += delta,
+//      trainer.cpp:198-204) and context updates c_r += sum_k g_kr s_k.
+// Lifetime order (LIFETIME = true; the reference default sweep_samples,
+// trainer.cpp:133-154) runs the same window as an anti-diagonal wavefront with
+// the sample rows in registers.
 // The 2W_f+1 ring of syn0 rows (ContextRing, trainer.cpp:32-102) stays in
-// registers for the sentence's lifetime and slides by register renaming.
-// Positions that the reference keeps resident until finish() (the last 2W_f+1)
-// are parked in shared memory and written back in ring-slot order, so each
-// sentence's global write sequence is the reference's.
+// registers for the sentence's lifetime and slides by register renaming; rows
+// leave it by overwrite (no shared-memory ring), as red.add deltas, or — the
+// exact mode — in the reference's write order with the finish() slot order.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -90,7 +92,6 @@ struct Butterfly {
     }
 };
 
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
