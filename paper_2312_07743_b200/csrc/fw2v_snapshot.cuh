@@ -886,7 +886,9 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
         return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, false>(blocks, m, b, n_neg, ctr, st, resident)
                     : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, false>(blocks, m, b, n_neg, ctr, st, resident);
     }
-    if constexpr (VEC > 10) {  // lifetime order: the window's sample rows would not fit in registers
+    if constexpr (NC < 6) {  // 4-sample chunks are only dispatched for N + 1 > 6
+        return cudaErrorInvalidValue;
+    } else if constexpr (VEC > 10) {  // lifetime order: the window's sample rows would not fit in registers
         if (lifetime) return cudaErrorInvalidValue;
         if (n_neg + 1 < NC) return launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
         return launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
