@@ -1,6 +1,7 @@
-"""Quality probe on the text8-shaped Zipf corpus (d=128, 1 epoch): SGNS loss of
-the reference CPU trainer vs the B200 trainer under several Hogwild settings.
-usage: python tools/quality_text8.py [dim] [config ...]   config = key=value,key=value"""
+"""Quality probe on the text8-shaped (or, with FW2V_SHAPE=1bw, the 1bw-shaped) Zipf
+corpus: SGNS loss of the reference CPU trainer vs the B200 trainer under several
+Hogwild settings.
+usage: python tools/quality_text8.py [dim] [epochs] [config ...]   config = key=value,key=value"""
 import os
 import sys
 import time
@@ -16,7 +17,7 @@ from oracle.oracle import Oracle, TrainConfig as RConfig  # noqa: E402
 dim = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 configs = sys.argv[3:] or ["reuse_mode=window_snapshot"]
-c = fw.synth_zipf(**fw.TEXT8_SHAPE)
+c = fw.synth_zipf(**(fw.ONEBW_SHAPE if os.environ.get("FW2V_SHAPE") == "1bw" else fw.TEXT8_SHAPE))
 counts, offsets, ids = c.counts, c.offsets, c.ids
 p = counts.astype(np.float64) ** 0.75
 negs = np.random.default_rng(5).choice(len(counts), 400_000 * 5, p=p / p.sum()).astype(np.int32)
