@@ -559,7 +559,8 @@ struct Slot {
 };
 
 struct Lane {
-    cudaStream_t stream = nullptr;  // kernels
+    cudaStream_t stream = nullptr;  // kernels of slot 0
+    cudaStream_t stream2 = nullptr; // kernels of slot 1 (Hogwild: a lane's sub-batches overlap)
     cudaStream_t copy = nullptr;    // H2D of the next sub-batch, overlapping the current kernel
     DevCounters* d_ctr = nullptr;
     Slot slot[2];
@@ -656,6 +657,16 @@ struct fw2v_ctx {
 
     // Hogwild sentences in flight per stream (0 = no cap): a batch larger than
     // the cap runs as consecutive launches on its stream.
+    // Hogwild: each lane runs its two slots' kernels on two streams, so a lane's
+    // next sub-batch starts while the previous one's last sentences finish.
+    int kernel_streams() const {
+        static const int env = [] {
+            const char* e = std::getenv("FW2V_KSTREAMS");  // experiments
+            return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+        }();
+        return deterministic ? 1 : env;
+    }
+
     int64_t inflight_per_stream(int streams) const {
         if (inflight_total <= 0) return 0;
         return std::max<int64_t>(1, inflight_total / std::max(1, streams));
@@ -704,6 +715,7 @@ struct fw2v_ctx {
         for (int i = 0; i < n; ++i) {
             Lane& ln = lanes[static_cast<size_t>(i)];
             if (!ln.stream) FW2V_CK(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+            if (!ln.stream2) FW2V_CK(cudaStreamCreateWithFlags(&ln.stream2, cudaStreamNonBlocking));
             if (!ln.copy) FW2V_CK(cudaStreamCreateWithFlags(&ln.copy, cudaStreamNonBlocking));
             if (!ln.d_ctr) FW2V_CK(cudaMalloc(&ln.d_ctr, sizeof(DevCounters)));
             if (ln.cap_words >= cap_words && ln.cap_sent >= cap_sent) continue;
@@ -729,10 +741,12 @@ struct fw2v_ctx {
         cudaSetDevice(cfg.device);
         for (Lane& ln : lanes) {
             if (ln.stream) cudaStreamSynchronize(ln.stream);
+            if (ln.stream2) cudaStreamSynchronize(ln.stream2);
             if (ln.copy) cudaStreamSynchronize(ln.copy);
             ln.release();
             cudaFree(ln.d_ctr);
             if (ln.stream) cudaStreamDestroy(ln.stream);
+            if (ln.stream2) cudaStreamDestroy(ln.stream2);
             if (ln.copy) cudaStreamDestroy(ln.copy);
         }
         cudaFree(hot_alloc);
@@ -1077,9 +1091,19 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
         x->ensure_lanes(P, cap_w, cap_s);
         // Sub-batches of ~256-511 sentences (equal parts of a chunk; enough to keep
         // the device full across the streams), never above S.
-        const uint64_t parts = std::max<uint64_t>(1, chunk / 256);
+        static const uint64_t sub_target = [] {
+            const char* e = std::getenv("FW2V_SUB_TARGET");  // experiments
+            return e ? std::max<uint64_t>(1, static_cast<uint64_t>(std::atoll(e))) : uint64_t{256};
+        }();
+        const uint64_t parts = std::max<uint64_t>(1, chunk / sub_target);
         const uint64_t sub = x->deterministic ? cfg.batch_sentences
                                               : std::min<uint64_t>(cfg.batch_sentences, (chunk + parts - 1) / parts);
+        static const uint64_t first_sub_env = [] {
+            const char* e = std::getenv("FW2V_FIRST_SUB");  // experiments
+            return e ? static_cast<uint64_t>(std::atoll(e)) : uint64_t{64};
+        }();
+        const uint64_t first_sub = x->deterministic ? 0 : first_sub_env;
+        const int KS = x->kernel_streams();  // kernel streams per lane
         const uint64_t schedule_total =
             cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
         const Sampler sp = x->sampler();
@@ -1101,11 +1125,14 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
             ~EvGuard() { cudaEventDestroy(e); }
         } ev_guard{synced};
         for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
-            for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), x->lanes[static_cast<size_t>(p)].stream));
-            if (!x->deterministic && x->hot_k > 0) {
-                x->hot_sync(false, x->lanes[0].stream);
-                FW2V_CK(cudaEventRecord(synced, x->lanes[0].stream));
-                for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, synced, 0));
+            // Counters cleared and hot replicas broadcast on lane 0's stream; every
+            // kernel stream starts after them.
+            for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), x->lanes[0].stream));
+            if (!x->deterministic && x->hot_k > 0) x->hot_sync(false, x->lanes[0].stream);
+            FW2V_CK(cudaEventRecord(synced, x->lanes[0].stream));
+            for (int p = 0; p < P; ++p) {
+                if (p > 0) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, synced, 0));
+                if (KS > 1) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream2, synced, 0));
             }
             std::atomic<uint64_t> reserved{x->words_trained};
             // FW2V_TRACE=1: per sub-batch host and device timeline on stderr (diagnostics).
@@ -1160,7 +1187,7 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                             uint64_t words = 0;
                             const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
                             // A short first sub-batch per thread gets the device busy early.
-                            const uint64_t want = std::min(left, which == 0 && wsum == 0 && !x->deterministic ? std::min<uint64_t>(sub, 64) : sub);
+                            const uint64_t want = std::min(left, which == 0 && wsum == 0 && first_sub > 0 ? std::min<uint64_t>(sub, first_sub) : sub);
                             const uint64_t kept = assemble(corpus, cursor, end, want, sp, rng, bo, &words);
                             left -= kept;
                             // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
@@ -1182,7 +1209,7 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                             }
                             // H2D on the lane's copy stream once the kernel that last read
                             // this slot's device buffers is done; the kernel waits for the copy.
-                            cudaStream_t st = ln.stream, cs = ln.copy;
+                            cudaStream_t st = which == 1 && KS > 1 ? ln.stream2 : ln.stream, cs = ln.copy;
                             if (sl.in_flight) FW2V_CK(cudaStreamWaitEvent(cs, sl.used, 0));
                             FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, cs));
                             if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, cs));
@@ -1201,7 +1228,7 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                                 FW2V_CK(cudaEventCreate(&rec.k1));
                                 FW2V_CK(cudaEventRecord(rec.k0, st));
                             }
-                            FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, P));
+                            FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, KS * P));
                             FW2V_CK(cudaEventRecord(sl.used, st));
                             if (trace) {
                                 FW2V_CK(cudaEventRecord(rec.k1, st));
@@ -1219,7 +1246,10 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                 });
             }
             for (auto& t : threads) t.join();
-            for (int p = 0; p < P; ++p) FW2V_CK(cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream));
+            for (int p = 0; p < P; ++p) {
+                FW2V_CK(cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream));
+                FW2V_CK(cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream2));
+            }
             if (!x->deterministic && x->hot_k > 0) {
                 x->hot_sync(true, x->lanes[0].stream);
                 FW2V_CK(cudaStreamSynchronize(x->lanes[0].stream));
@@ -1395,7 +1425,11 @@ int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* 
         const bool hot = !x->deterministic && x->hot_k > 0;
         if (hot) x->hot_sync(false, s0);
         FW2V_CK(cudaEventRecord(fork, s0));
-        for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, fork, 0));
+        const int KS = x->kernel_streams();
+        for (int p = 0; p < P; ++p) {
+            if (p > 0) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, fork, 0));
+            if (KS > 1) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream2, fork, 0));
+        }
         // Interleave launches across lanes so each stream always has queued work.
         size_t maxb = 0;
         for (auto& l : plan->lanes) maxb = std::max(maxb, l.size());
@@ -1403,8 +1437,16 @@ int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* 
             for (int p = 0; p < P; ++p)
                 if (k < plan->lanes[static_cast<size_t>(p)].size())
                     FW2V_CK(x->launch(plan->lanes[static_cast<size_t>(p)][k].view, x->deterministic,
-                                      x->lanes[static_cast<size_t>(p)].d_ctr, x->lanes[static_cast<size_t>(p)].stream, P));
-        for (int p = 0; p < P; ++p) FW2V_CK(cudaEventRecord(ends[static_cast<size_t>(p)], x->lanes[static_cast<size_t>(p)].stream));
+                                      x->lanes[static_cast<size_t>(p)].d_ctr,
+                                      (k & 1) && KS > 1 ? x->lanes[static_cast<size_t>(p)].stream2 : x->lanes[static_cast<size_t>(p)].stream,
+                                      KS * P));
+        for (int p = 0; p < P; ++p) {
+            if (KS > 1) {  // join the lane's second kernel stream
+                FW2V_CK(cudaEventRecord(ends[static_cast<size_t>(p)], x->lanes[static_cast<size_t>(p)].stream2));
+                FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, ends[static_cast<size_t>(p)], 0));
+            }
+            FW2V_CK(cudaEventRecord(ends[static_cast<size_t>(p)], x->lanes[static_cast<size_t>(p)].stream));
+        }
         if (hot) {
             // Join every lane on s0, fold the replicas back; the pass ends there.
             for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(s0, ends[static_cast<size_t>(p)], 0));
