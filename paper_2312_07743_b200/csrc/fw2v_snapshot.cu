@@ -4,7 +4,7 @@
 
 namespace fw2v {
 
-#define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(16, 8) X(32, 4) X(32, 6) X(32, 8) X(32, 10) X(32, 12) X(32, 16)
+#define FW2V_K1S_SHAPES(X) X(4, 4) X(8, 4) X(16, 4) X(16, 8) X(32, 4) X(32, 6) X(32, 8) X(32, 10) X(32, 12) X(32, 16) X(64, 8)
 
 #define FW2V_EXTERN(L_, V_)                                                                                 \
     extern template cudaError_t launch_k1s_shape<L_, V_>(const ModelView&, const BatchView&, int, int, bool, bool, \
@@ -27,6 +27,7 @@ cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& 
 bool k1s_supported(int lanes, int vec, int n_neg, int wf, bool lifetime) {
     if (n_neg < 0 || wf < 1 || wf > 5 || (!lifetime && n_neg + 1 > kMaxSnapSamples)) return false;
     if (lifetime && vec > 10) return false;  // the window's sample rows no longer fit in registers
+    if (lifetime && lanes > 32) return false;  // two-warp groups: window-snapshot order only
 #define FW2V_CASE(L_, V_) if (lanes == L_ && vec == V_) return true;
     FW2V_K1S_SHAPES(FW2V_CASE)
 #undef FW2V_CASE

@@ -110,6 +110,14 @@ struct K1sSmem {
     static constexpr int NV = NC * NCTX;
     static constexpr int GPAD = (NV + 3) & ~3;
     static constexpr int STRIDE = LANES * VEC;
+    // LANES = 64 (d = 512 as 64 x 8): one sentence on the block's two warps, each
+    // owning half of the columns. Control logic and the butterfly run per warp
+    // (CL lanes); the two warps' partial dots meet in a double-buffered exchange.
+    static constexpr int CL = LANES > 32 ? 32 : LANES;
+    static constexpr int NWG = LANES / CL;  // warps per group
+    static constexpr int NFX = (Butterfly<CL / 2, NV>::final_count() + 3) & ~3;
+    static constexpr int XB = NWG > 1 ? 2 * NWG * NFX * 32 : 0;
+    static constexpr int GA = NWG * GPAD + XB;  // g areas (one per warp) + exchange
     // Wide lane slices (VEC >= 8) hold twice the registers per lane: 64-thread
     // blocks keep the per-block shared memory small enough for 5 blocks per SM.
     static constexpr int THREADS = VEC >= 8 ? 64 : kK1Threads;
@@ -119,7 +127,7 @@ struct K1sSmem {
     // RING = false (Hogwild overwrite write-back): ring rows leave straight to HBM,
     // no shared-memory ring: 64% of the footprint, 6 blocks per SM at d=128.
     static constexpr int SROWS = SNAPALL ? (kMaxSnapSamples > 2 * NC ? kMaxSnapSamples : 2 * NC) : 2 * NC;
-    static constexpr int kGroupFloats = GPAD + SROWS * STRIDE + (RING ? C * STRIDE : 0);
+    static constexpr int kGroupFloats = GA + SROWS * STRIDE + (RING ? C * STRIDE : 0);
     static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
     // Register budget (blocks per SM the compiler must fit): 168 registers at
@@ -275,7 +283,8 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
     constexpr int NV = SM::NV;
     constexpr int H2 = VEC / 2;
     constexpr int STRIDE = SM::STRIDE;
-    constexpr int HALF = LANES / 2;
+    constexpr int CL = SM::CL;      // control lanes: the group, or one warp of a 64-lane group
+    constexpr int HALF = CL / 2;
     constexpr int NN = NC - 1;  // negatives per window held by every lane (single-chunk path)
     // Stale-prefetch detection by one __match_any_sync: lanes q < NC of a group
     // carry this window's sample ids, lanes HALF + q the previous window's.
@@ -285,19 +294,24 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
     // that level needs no selects.
     constexpr bool kPreswap = NC % 2 == 0;
     using SL = Slice<H2, LANES>;
-    using BF = Butterfly<LANES / 2, NV>;
+    using BF = Butterfly<CL / 2, NV>;
     constexpr int NF = BF::final_count();
     static_assert(NV <= 255 && NC <= 16 && NCTX <= 16, "slot words");
     extern __shared__ __align__(16) float k1s_sh[];
 
     const int lane = threadIdx.x & 31;
-    const int sub = lane & (LANES - 1);
-    const int grp = lane / LANES;
+    const int sub = static_cast<int>(threadIdx.x) & (LANES - 1);  // column slice
+    const int csub = lane & (CL - 1);                               // control / butterfly lane
+    const int grp = lane / CL;
+    const int wig = static_cast<int>(threadIdx.x >> 5) & (SM::NWG - 1);  // warp in group
     const int sent = static_cast<int>((blockIdx.x * SM::THREADS + threadIdx.x) / LANES);
     const bool has = sent < b.n_sentences;
-    float* gsh = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
-    float* sbuf = gsh + SM::GPAD + sub * SL::CW;                  // + (parity*NC + q)*STRIDE
-    float* ring = gsh + SM::GPAD + SM::SROWS * STRIDE + sub * SL::CW;  // + slot*STRIDE
+    float* gbase = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
+    float* gsh = gbase + wig * SM::GPAD;
+    [[maybe_unused]] float* xbuf = gbase + SM::NWG * SM::GPAD;     // + (parity*NWG + warp)*NFX*32
+    float* sbuf = gbase + SM::GA + sub * SL::CW;                    // + (parity*NC + q)*STRIDE
+    float* ring = gbase + SM::GA + SM::SROWS * STRIDE + sub * SL::CW;  // + slot*STRIDE
+    [[maybe_unused]] unsigned xpar = 0;
     const bool delta_wb = RING && (m.flags & kFlagDeltaRing) != 0;
 
     uint32_t beg = 0, len = 0;
@@ -332,7 +346,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
         int idx[NV];
 #pragma unroll
         for (int j = 0; j < NV; ++j) idx[j] = j;
-        BF::plan(idx, sub);
+        BF::plan(idx, csub);
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
             const int q = idx[j] / NCTX, r = idx[j] - q * NCTX;
@@ -341,7 +355,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
             asm volatile("" : "+r"(slotw[j]));
         }
     }
-    const int swap_off = (kPreswap && (sub & HALF) != 0) ? (NC / 2) * STRIDE : 0;
+    const int swap_off = (kPreswap && (csub & HALF) != 0) ? (NC / 2) * STRIDE : 0;
 
     float2 ctx[NCTX][H2];
     int tok[NCTX];
@@ -432,12 +446,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
             // This window's rows the previous window rewrote after their prefetch
             // was issued (computed here, off the critical path).
             if constexpr (kMatch) {
-                const int q = sub & (HALF - 1);
+                const int q = csub & (HALF - 1);
                 int cv = ttok;
 #pragma unroll
                 for (int k = 0; k < NN; ++k) cv = q == k + 1 ? ncur[k] : cv;
                 cv = (wact && q <= n_neg && q < NC) ? cv : -1 - lane;
-                const int mv = sub < HALF ? cv : prev_v;
+                const int mv = csub < HALF ? cv : prev_v;
                 match_mask = __match_any_sync(kFull, mv);  // consumed after the wait below
                 prev_v = cv;
             } else {
@@ -514,12 +528,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 // without a sample hold finite stale rows and get g = 0.
                 KB_T(0)
                 if constexpr (kMatch) {  // the match issued at the top of the window has landed
-                    const unsigned upper = ((1u << HALF) - 1u) << (grp * LANES + HALF);
-                    const bool st = sub < HALF && (match_mask & upper) != 0u;
-                    stale = (__ballot_sync(kFull, st) >> (grp * LANES)) & ((1u << NC) - 1u);
+                    const unsigned upper = ((1u << HALF) - 1u) << (grp * CL + HALF);
+                    const bool st = csub < HALF && (match_mask & upper) != 0u;
+                    stale = (__ballot_sync(kFull, st) >> (grp * CL)) & ((1u << NC) - 1u);
                     if constexpr (LIFETIME) {
-                        const unsigned lower = ((1u << HALF) - 1u) << (grp * LANES);
-                        dup = __any_sync(kFull, sub < HALF && __popc(match_mask & lower) > 1);
+                        const unsigned lower = ((1u << HALF) - 1u) << (grp * CL);
+                        dup = __any_sync(kFull, csub < HALF && __popc(match_mask & lower) > 1);
                     }
                 }
                 cp_async_wait_group<1>();
@@ -657,8 +671,21 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                 }
             }
             KB_T(3)
-            if constexpr (kPreswap) BF::reduce_preswapped(P, sub);
-            else BF::reduce(P, sub);
+            if constexpr (kPreswap) BF::reduce_preswapped(P, csub);
+            else BF::reduce(P, csub);
+            if constexpr (SM::NWG > 1) {
+                // Both warps' column halves: the exchange buffer is double-buffered,
+                // so one barrier per chunk orders every reuse. Sentence-uniform
+                // control flow: both warps reach each barrier.
+                float* mine = xbuf + (xpar * SM::NWG + wig) * SM::NFX * 32 + lane;
+                const float* other = xbuf + (xpar * SM::NWG + (wig ^ 1)) * SM::NFX * 32 + lane;
+#pragma unroll
+                for (int j = 0; j < NF; ++j) mine[j * 32] = P[j];
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < NF; ++j) P[j] += other[j * 32];
+                xpar ^= 1u;
+            }
 
             KB_T(4)
             // 3. sigmoid on the owned dots; g published as scalars [q][r].
@@ -874,6 +901,15 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
                           DevCounters* ctr, cudaStream_t st, int* resident) {
     constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;  // RING does not change THREADS
     const int blocks = (b.n_sentences + per_block - 1) / per_block;
+    if constexpr (LANES > 32) {  // 64-lane groups: window-snapshot order only
+        if (lifetime) return cudaErrorInvalidValue;
+        if (n_neg + 1 > NC)
+            return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, false>(blocks, m, b, n_neg, ctr, st, resident)
+                        : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, false>(blocks, m, b, n_neg, ctr, st, resident);
+        if constexpr (NC < 6) return cudaErrorInvalidValue;
+        else if (n_neg + 1 < NC) return launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+        else return launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+    } else {
     if (n_neg + 1 > NC) {
         // Chunks of NC samples; in lifetime order each chunk is its own wavefront,
         // started from the contexts the previous chunk left (exact order).
@@ -898,6 +934,7 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
                             : launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
         return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
                         : launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+    }
     }
 }
 

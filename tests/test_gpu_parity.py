@@ -174,7 +174,7 @@ def _disjoint_batch(n, L, pool, n_neg, seed, distinct=False):
     return counts, offsets, ids, negs
 
 
-@pytest.mark.parametrize("dim", [16, 32, 64, 128, 256, 300])
+@pytest.mark.parametrize("dim", [16, 32, 64, 128, 256, 300, 512])
 @pytest.mark.parametrize("delta", [False, True])
 def test_k1s_disjoint_batch_equals_serial(oracle, dim, delta):
     """A whole Hogwild K1s batch (several sentences per warp at small lane
@@ -229,7 +229,7 @@ def test_k1s_hot_replicas_average(oracle, replicas):
     assert np.abs(go - want).max() <= 2e-5 * np.abs(ro).max() + 1e-7
 
 
-@pytest.mark.parametrize("dim", [32, 64, 128, 300])
+@pytest.mark.parametrize("dim", [32, 64, 128, 300, 512])
 def test_k1s_overwrite_without_ring_matches_delta(dim):
     """delta_writeback=2 (ring rows stored straight back, no shared-memory ring;
     fast-sigmoid kernels) equals the delta write-back on row-disjoint sentences
@@ -254,7 +254,8 @@ def test_k1s_overwrite_without_ring_matches_delta(dim):
 
 @pytest.mark.parametrize("mode", ["lifetime", "window_snapshot"])
 @pytest.mark.parametrize("dim,window,n_neg", [(128, 5, 0), (128, 5, 2), (128, 5, 15), (32, 5, 15), (128, 9, 15),
-                                              (64, 3, 9), (300, 5, 11), (512, 5, 5)])
+                                              (64, 3, 9), (300, 5, 11), (512, 5, 5), (512, 3, 5), (512, 5, 15),
+                                              (512, 9, 15), (512, 9, 5), (512, 1, 2)])
 def test_k1s_negative_counts_single_sentence(oracle, mode, dim, window, n_neg):
     """K1s with any number of negatives (partial chunk, several chunks per window;
     lifetime order: one wavefront per chunk) == the reference order per sentence,

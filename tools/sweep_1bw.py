@@ -29,8 +29,10 @@ with open("/proc/meminfo") as f:
 print(f"# host MemAvailable {avail_gb:.0f} GB", flush=True)
 
 modes = sys.argv[1].split(",") if len(sys.argv) > 1 else ["window_snapshot", "lifetime"]
-grid = [(d, w, n, 10000) for d in (64, 128, 256, 512) for w in (2, 5, 8) for n in (5, 15)]
-grid += [(128, 5, 5, 1000), (128, 5, 5, 50000)]
+dims = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [64, 128, 256, 512]
+grid = [(d, w, n, 10000) for d in dims for w in (2, 5, 8) for n in (5, 15)]
+if 128 in dims:
+    grid += [(128, 5, 5, 1000), (128, 5, 5, 50000)]
 for mode in modes:
     for d, w, n, S in grid:
         if n == 15 and avail_gb < 120:  # the host-side plan of an N=15 epoch is ~34 GB
