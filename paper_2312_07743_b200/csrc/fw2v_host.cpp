@@ -497,7 +497,7 @@ Shape choose_shape(int dim, int lanes_pref) {
 // sentences per warp amortise the per-window butterfly, sigmoid and
 // bookkeeping) with at most 8 columns per lane when the stride allows it
 // (registers), up to 16 on 32 lanes for wide rows (d = 300 -> 32 x 10); d = 512 runs on two
-// warps per sentence (64 x 8) in window-snapshot order, 32 x 16 in lifetime order (K1).
+// warps per sentence (64 x 8).
 Shape choose_k1s_shape(int stride, const Shape& k1, int lanes_pref, int n_neg, int wf, bool lifetime) {
     if (lanes_pref == 0) {
         static const Shape pref[] = {{4, 4}, {8, 4}, {16, 4}, {16, 8}, {32, 4}, {32, 6}, {32, 8}, {32, 10}, {32, 12},

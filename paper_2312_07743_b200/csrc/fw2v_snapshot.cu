@@ -27,7 +27,6 @@ cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& 
 bool k1s_supported(int lanes, int vec, int n_neg, int wf, bool lifetime) {
     if (n_neg < 0 || wf < 1 || wf > 5 || (!lifetime && n_neg + 1 > kMaxSnapSamples)) return false;
     if (lifetime && vec > 10) return false;  // the window's sample rows no longer fit in registers
-    if (lifetime && lanes > 32) return false;  // two-warp groups: window-snapshot order only
 #define FW2V_CASE(L_, V_) if (lanes == L_ && vec == V_) return true;
     FW2V_K1S_SHAPES(FW2V_CASE)
 #undef FW2V_CASE

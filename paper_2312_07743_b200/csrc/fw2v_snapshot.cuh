@@ -115,7 +115,8 @@ struct K1sSmem {
     // (CL lanes); the two warps' partial dots meet in a double-buffered exchange.
     static constexpr int CL = LANES > 32 ? 32 : LANES;
     static constexpr int NWG = LANES / CL;  // warps per group
-    static constexpr int NFX = (Butterfly<CL / 2, NV>::final_count() + 3) & ~3;
+    // exchange slots per lane: the butterfly's outputs, or a wavefront step's NC dots
+    static constexpr int NFX = ((Butterfly<CL / 2, NV>::final_count() > NC ? Butterfly<CL / 2, NV>::final_count() : NC) + 3) & ~3;
     static constexpr int XB = NWG > 1 ? 2 * NWG * NFX * 32 : 0;
     static constexpr int GA = NWG * GPAD + XB;  // g areas (one per warp) + exchange
     // Wide lane slices (VEC >= 8) hold twice the registers per lane: 64-thread
@@ -600,6 +601,22 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                     for (int h = 1; h < H2; ++h) acc = __ffma2_rn(ctx[j][h], S[k][h], acc);
                     return acc.x + acc.y;
                 };
+                // 64-lane groups: the two warps' partial dots of one step meet in the
+                // double-buffered exchange (one barrier per step; sentence-uniform).
+                auto exchange = [&](float* f, auto live) {
+                    if constexpr (SM::NWG > 1) {
+                        float* mine = xbuf + (xpar * SM::NWG + wig) * SM::NFX * 32 + lane;
+                        const float* other = xbuf + (xpar * SM::NWG + (wig ^ 1)) * SM::NFX * 32 + lane;
+#pragma unroll
+                        for (int k = 0; k < NC; ++k)
+                            if (live(k)) mine[k * 32] = f[k];
+                        __syncthreads();
+#pragma unroll
+                        for (int k = 0; k < NC; ++k)
+                            if (live(k)) f[k] += other[k * 32];
+                        xpar ^= 1u;
+                    }
+                };
                 if (!dup) {
                     // Anti-diagonal d: pairings (k, d-k), independent of each other.
 #pragma unroll
@@ -609,10 +626,11 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                         for (int k = 0; k < NC; ++k)
                             if (d - k >= 0 && d - k < NCTX) f[k] = dot(k, d - k);
 #pragma unroll
-                        for (int o = LANES / 2; o > 0; o >>= 1)
+                        for (int o = CL / 2; o > 0; o >>= 1)
 #pragma unroll
                             for (int k = 0; k < NC; ++k)
                                 if (d - k >= 0 && d - k < NCTX) f[k] += __shfl_xor_sync(kFull, f[k], o);
+                        exchange(f, [&](int k) { return d - k >= 0 && d - k < NCTX; });
                         // (g evaluated by every lane: a lane-distributed sigmoid with
                         // shuffled g measured 7% slower; the wavefront is latency-bound)
 #pragma unroll
@@ -629,10 +647,11 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
                             if (sid[k2] == sid[k]) vcopy2(S[k], S[k2]);
 #pragma unroll
                         for (int j = 0; j < NCTX; ++j) {
-                            float f = dot(k, j);
+                            float f[1] = {dot(k, j)};
 #pragma unroll
-                            for (int o = LANES / 2; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
-                            update(k, j, pair_g(k, j, f));
+                            for (int o = CL / 2; o > 0; o >>= 1) f[0] += __shfl_xor_sync(kFull, f[0], o);
+                            exchange(f, [](int kk) { return kk == 0; });
+                            update(k, j, pair_g(k, j, f[0]));
                         }
                     }
                 }
@@ -901,15 +920,6 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
                           DevCounters* ctr, cudaStream_t st, int* resident) {
     constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;  // RING does not change THREADS
     const int blocks = (b.n_sentences + per_block - 1) / per_block;
-    if constexpr (LANES > 32) {  // 64-lane groups: window-snapshot order only
-        if (lifetime) return cudaErrorInvalidValue;
-        if (n_neg + 1 > NC)
-            return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, false>(blocks, m, b, n_neg, ctr, st, resident)
-                        : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, false>(blocks, m, b, n_neg, ctr, st, resident);
-        if constexpr (NC < 6) return cudaErrorInvalidValue;
-        else if (n_neg + 1 < NC) return launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
-        else return launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
-    } else {
     if (n_neg + 1 > NC) {
         // Chunks of NC samples; in lifetime order each chunk is its own wavefront,
         // started from the contexts the previous chunk left (exact order).
@@ -934,7 +944,6 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
                             : launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
         return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
                         : launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
-    }
     }
 }
 

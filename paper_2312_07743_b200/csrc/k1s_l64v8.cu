@@ -1,5 +1,5 @@
-// K1s instantiation for 64 lanes x 8 columns: d = 512 on two warps per sentence
-// (window-snapshot order), one translation unit per shape.
+// K1s instantiation for 64 lanes x 8 columns: d = 512 on two warps per sentence,
+// one translation unit per shape.
 #include "fw2v_snapshot.cuh"
 
 namespace fw2v {
