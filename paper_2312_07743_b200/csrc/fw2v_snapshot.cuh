@@ -23,6 +23,9 @@
 // registers for the sentence's lifetime and slides by register renaming; rows
 // leave it by overwrite (no shared-memory ring), as red.add deltas, or — the
 // exact mode — in the reference's write order with the finish() slot order.
+// A lane group is 4-32 lanes of one warp (several sentences per warp), or at
+// d = 512 the block's two warps (64 lanes x 8 columns): the butterfly runs per
+// warp and the two halves' partial dots meet in a shared-memory exchange.
 #pragma once
 
 #include <cuda_runtime.h>
