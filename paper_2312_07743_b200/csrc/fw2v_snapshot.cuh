@@ -130,7 +130,10 @@ struct K1sSmem {
     // (delta write-back) or the finish() stash (overwrite) — never both.
     // RING = false (Hogwild overwrite write-back): ring rows leave straight to HBM,
     // no shared-memory ring: 64% of the footprint, 6 blocks per SM at d=128.
-    static constexpr int SROWS = SNAPALL ? (kMaxSnapSamples > 2 * NC ? kMaxSnapSamples : 2 * NC) : 2 * NC;
+    // SNAPALL: every chunk's NC slots, the last chunk's unused ones included
+    // (its dots read all NC slots; their g is 0).
+    static constexpr int SNAP_ROWS = (kMaxSnapSamples + NC - 1) / NC * NC;
+    static constexpr int SROWS = SNAPALL ? (SNAP_ROWS > 2 * NC ? SNAP_ROWS : 2 * NC) : 2 * NC;
     static constexpr int kGroupFloats = GA + SROWS * STRIDE + (RING ? C * STRIDE : 0);
     static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
