@@ -303,8 +303,8 @@ def run_ours(args, world, rank, local, dist):
                          "bytes_per_word": bpw,
                          "note": "algorithmic lifetime-mode bytes/word x words/s; the model is L2-resident "
                                  "so frac can exceed 1 (ncu: ~124 B of DRAM traffic per word). The kernel is "
-                                 "issue/L1-bound: 496 warp-instructions per word against an FFMA2 floor of 216, "
-                                 "issue 53%, FMA pipe 54%, L1 wavefronts 73% (profiles/r01j_k1s_snapshot_quick.txt)"},
+                                 "issue/L1-bound: 492 warp-instructions per word against an FFMA2 floor of 216, "
+                                 "issue 53%, FMA pipe 53%, L1 wavefronts 73% (profiles/r01l_k1s_snapshot_quick.txt)"},
             "e2e": e2e, "gpu_launches": (n_launches + (2 if cfg.hot_rows > 0 else 0)) * args.steps, "clocks": clocks,
             "wall_s_timed": wall,
         }
