@@ -953,13 +953,29 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
     }
 }
 
+// Window-snapshot multi-chunk kernels only (N + 1 > NC).
+template <int LANES, int VEC, int WF, int NC>
+cudaError_t launch_k1s_snap_multi(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
+                                  cudaStream_t st, int* resident) {
+    constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;
+    const int blocks = (b.n_sentences + per_block - 1) / per_block;
+    return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, false>(blocks, m, b, n_neg, ctr, st, resident)
+                : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, false>(blocks, m, b, n_neg, ctr, st, resident);
+}
+
 template <int LANES, int VEC>
 cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast, bool lifetime,
                              DevCounters* ctr, cudaStream_t st, int* resident) {
+    // Window-snapshot order at W_f = 3 with 13-16 samples: two 8-sample chunks
+    // instead of three of 6 (fewer butterflies; measured +3-8% at N=15, 1bw shape;
+    // lifetime order keeps 6: its 8-sample wavefront spills).
+    const int S = n_neg + 1;
+    const bool nc8 = !lifetime && S > 8 && (S + 7) / 8 < (S + 5) / 6;
     switch (wf) {
     case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
     case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
-    case 3: return launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
+    case 3: return nc8 ? launch_k1s_snap_multi<LANES, VEC, 3, 8>(m, b, n_neg, fast, ctr, st, resident)
+                       : launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
     // Wide windows: one 6-sample chunk when N+1 <= 6, else 4-sample chunks (registers).
     case 4: return n_neg + 1 <= 6 ? launch_k1s_nc<LANES, VEC, 4, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident)
                                   : launch_k1s_nc<LANES, VEC, 4, 4>(m, b, n_neg, fast, lifetime, ctr, st, resident);
