@@ -1,4 +1,4 @@
-"""Experiment: 8-sample chunks (FW2V_K1S_NC8) vs 6 at W=5, N=15 on the 1bw shape."""
+"""W=5, N=11/15 throughput on the 1bw shape (used to choose 8- vs 6-sample chunks; the FW2V_K1S_NC8 switch it compared is gone: 8-sample chunks are now picked automatically)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2312_07743_b200 as fw
