@@ -966,14 +966,16 @@ cudaError_t launch_k1s_snap_multi(const ModelView& m, const BatchView& b, int n_
 template <int LANES, int VEC>
 cudaError_t launch_k1s_shape(const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast, bool lifetime,
                              DevCounters* ctr, cudaStream_t st, int* resident) {
-    // Window-snapshot order at W_f = 3 with 13-16 samples: two 8-sample chunks
+    // Window-snapshot order at W_f <= 3 with 13-16 samples: two 8-sample chunks
     // instead of three of 6 (fewer butterflies; measured +3-8% at N=15, 1bw shape;
     // lifetime order keeps 6: its 8-sample wavefront spills).
     const int S = n_neg + 1;
     const bool nc8 = !lifetime && S > 8 && (S + 7) / 8 < (S + 5) / 6;
     switch (wf) {
-    case 1: return launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
-    case 2: return launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
+    case 1: return nc8 ? launch_k1s_snap_multi<LANES, VEC, 1, 8>(m, b, n_neg, fast, ctr, st, resident)
+                       : launch_k1s_nc<LANES, VEC, 1, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
+    case 2: return nc8 ? launch_k1s_snap_multi<LANES, VEC, 2, 8>(m, b, n_neg, fast, ctr, st, resident)
+                       : launch_k1s_nc<LANES, VEC, 2, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
     case 3: return nc8 ? launch_k1s_snap_multi<LANES, VEC, 3, 8>(m, b, n_neg, fast, ctr, st, resident)
                        : launch_k1s_nc<LANES, VEC, 3, 6>(m, b, n_neg, fast, lifetime, ctr, st, resident);
     // Wide windows: one 6-sample chunk when N+1 <= 6, else 4-sample chunks (registers).

@@ -255,7 +255,8 @@ def test_k1s_overwrite_without_ring_matches_delta(dim):
 @pytest.mark.parametrize("mode", ["lifetime", "window_snapshot"])
 @pytest.mark.parametrize("dim,window,n_neg", [(128, 5, 0), (128, 5, 2), (128, 5, 15), (32, 5, 15), (128, 9, 15),
                                               (64, 3, 9), (300, 5, 11), (512, 5, 5), (512, 3, 5), (512, 5, 15),
-                                              (512, 9, 15), (512, 9, 5), (512, 1, 2)])
+                                              (512, 9, 15), (512, 9, 5), (512, 1, 2), (128, 2, 15), (64, 3, 13),
+                                              (256, 2, 12)])
 def test_k1s_negative_counts_single_sentence(oracle, mode, dim, window, n_neg):
     """K1s with any number of negatives (partial chunk, several chunks per window;
     lifetime order: one wavefront per chunk) == the reference order per sentence,
