@@ -806,7 +806,7 @@ uint64_t expected_epoch_words(const fw2v_ctx& x) {  // trainer.cpp:378-386
 // lifts V_eff to ~9,700 there; the reference's 60-word pipeline test
 // (V_eff = 60, alpha 0.05) is held to 40 sentences.
 int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power, int n_neg, float alpha0, int hot_k,
-                      int hot_r) {
+                      int hot_r, int dim) {
     double z = 0.0, z2 = 0.0;
     for (int32_t w = 0; w < vocab_size; ++w) {
         const double p = std::pow(static_cast<double>(counts[w]), power);
@@ -814,7 +814,10 @@ int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power, 
         z2 += p * p / (w < hot_k ? hot_r : 1);  // a replicated row is shared by 1/R of the sentences
     }
     const double v_eff = z2 > 0.0 ? z * z / z2 : 1.0;
-    const double m = 8.0 * 0.025 * v_eff / ((n_neg + 1) * static_cast<double>(alpha0));
+    // Wide rows tolerate less staleness (measured on the planted corpus: d=512 at
+    // 888 sentences in flight +2.3% loss, at 512 +0.7%; d=128 fine at 3,552).
+    const double wide = dim > 128 ? (128.0 / dim) * (128.0 / dim) : 1.0;
+    const double m = 8.0 * 0.025 * v_eff / ((n_neg + 1) * static_cast<double>(alpha0)) * wide;
     return std::max<int64_t>(32, static_cast<int64_t>(std::ceil(m)));
 }
 
@@ -895,7 +898,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         x->k1_flags |= cfg->l1_refresh_log2 > 0 ? (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift) : kFlagL1Exact;
         if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments
         x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
-                            : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives, cfg->alpha0, 0, 1) : 0;
+                            : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives, cfg->alpha0, 0, 1, cfg->dim) : 0;
         x->deterministic = cfg->deterministic == 1 || (cfg->deterministic < 0 && x->cfg.workers == 1);
         x->shape = choose_shape(cfg->dim, cfg->k1_lanes);
         x->stride = row_stride_for(cfg->dim, cfg->k1_lanes);
@@ -927,7 +930,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
             x->place_hot();
             x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
                                 : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives,
-                                                                         cfg->alpha0, x->hot_k, x->hot_r)
+                                                                         cfg->alpha0, x->hot_k, x->hot_r, cfg->dim)
                                                          : 0;
         }
         if (x->inflight_total > 0 && !x->deterministic) {
