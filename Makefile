@@ -51,11 +51,16 @@ $(BUILD)/fw2v_io.o: $(SRC)/fw2v_io.cpp include/fw2v.h
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -O3 -c -o $@ $<
 
+# NCCL is opened at run time (dlopen); only its header is needed here.
+$(BUILD)/fw2v_nccl.o: $(SRC)/fw2v_nccl.cpp
+	@mkdir -p $(BUILD)
+	$(CXX) $(CXXFLAGS) -c -o $@ $<
+
 $(BUILD)/fw2v_corpus.o: $(SRC)/fw2v_corpus.cpp include/fw2v.h
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -O3 -c -o $@ $<
 
-$(LIB)/libfw2v.so: $(BUILD)/fw2v_kernels.o $(BUILD)/fw2v_snapshot.o $(K1S_OBJS) $(BUILD)/fw2v_host.o $(BUILD)/fw2v_corpus.o \
+$(LIB)/libfw2v.so: $(BUILD)/fw2v_kernels.o $(BUILD)/fw2v_snapshot.o $(K1S_OBJS) $(BUILD)/fw2v_host.o $(BUILD)/fw2v_corpus.o $(BUILD)/fw2v_nccl.o \
                    $(BUILD)/fw2v_io.o $(BUILD)/fw2v_eval.o
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread -ldl -lrt

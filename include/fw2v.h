@@ -113,7 +113,8 @@ typedef struct fw2v_report {
     int32_t n_epochs;
     fw2v_counters traffic;  /* instrumented on the device */
     fw2v_counters analytic; /* per-sentence closed forms (traffic.cpp:21-59) */
-    double kernel_seconds;  /* device time of the training kernels (CUDA events) */
+    double kernel_seconds;  /* device span of the training passes (CUDA events on the launching streams,
+                               pass start to last kernel completion), summed over passes */
     uint64_t h2d_bytes;     /* bytes copied host->device by the batch pipeline */
 } fw2v_report;
 
@@ -184,10 +185,57 @@ int fw2v_plan_epoch(fw2v_ctx* ctx, const uint64_t* offsets, uint64_t n_sentences
                     int32_t epoch, fw2v_plan** out);
 int fw2v_plan_info(const fw2v_plan* plan, uint64_t* words, uint64_t* sentences, uint64_t* batches,
                    uint64_t* device_bytes);
+/* The same for chunks [chunk_begin, chunk_end) of an n_chunks partition of the corpus
+ * (trainer.cpp:431-434; chunk p keeps its streams derive(seed, epoch, p, k)): one shard / one
+ * averaging round of a data-parallel job. alpha of local word w uses the schedule position
+ * words_base + (w - words_base) * words_scale (words_scale = shards per job / shards here). */
+int fw2v_plan_chunks(fw2v_ctx* ctx, const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids, int32_t epoch,
+                     int32_t n_chunks, int32_t chunk_begin, int32_t chunk_end, uint64_t words_base,
+                     int32_t words_scale, fw2v_plan** out);
 /* Launches the plan's kernels on the context's streams and waits; seconds =
  * CUDA-event device time from first launch to last completion. */
 int fw2v_plan_run(fw2v_ctx* ctx, fw2v_plan* plan, double* seconds, fw2v_counters* counters);
 void fw2v_plan_destroy(fw2v_plan* plan);
+
+/* ---- Data-parallel replicas (north_star "replicates syn0/syn1neg per GPU,
+ * shards the corpus, and averages the replicas periodically with an NCCL allreduce") ----
+ * The reference has one model shared by its worker threads (trainer.cpp:429-503); across GPUs each
+ * device holds a replica and the exchange step is the replica average. */
+
+/* In place: every context's syn0 and syn1 <- their element-wise mean over the n contexts (and, for
+ * a context joined with fw2v_comm_init_rank, over every process of its communicator).
+ * Contexts on distinct devices: one ncclAllReduce(ncclFloat32, ncclAvg) per matrix (libnccl.so.2,
+ * opened at run time; communicators cached per context set) over NVLink / NVSwitch. Contexts that
+ * share a device, FW2V_AVERAGE=peer, or no NCCL: a peer-memory kernel (member g reads slice g of
+ * every replica over P2P and writes the mean back into all of them). Synchronous; training on the
+ * contexts must not be in flight. FW2V_ERR_BAD_ARGUMENT if the replicas differ in shape. */
+int fw2v_average(fw2v_ctx* const* ctxs, int32_t n);
+/* Cross-process communicator (one process per GPU): rank 0 calls fw2v_nccl_unique_id, the caller
+ * distributes the 128 bytes (e.g. torch.distributed broadcast), every rank joins its context. */
+int fw2v_nccl_unique_id(uint8_t out[128]);
+int fw2v_comm_init_rank(fw2v_ctx* ctx, const uint8_t id[128], int32_t world, int32_t rank);
+
+/* Exchange across processes, called by fw2v_train_corpus_multi at every averaging point after this
+ * process's kernels finished and its own contexts were averaged: must average the replicas over
+ * all processes in place (e.g. torch.distributed all_reduce of attached model tensors) and set
+ * *global_words to the sum of local_words over processes. Returns 0 or an fw2v status. */
+typedef int (*fw2v_exchange_fn)(void* user, uint64_t local_words, uint64_t* global_words);
+
+/* Data-parallel training: this call trains shards shard0 .. shard0+n-1 (context i <- shard
+ * shard0+i) of an n_shards-shard job (n_shards > n: other processes hold the rest and `exchange`
+ * or fw2v_comm_init_rank connects them). The corpus is cut into the reference's producer chunks
+ * (cfg.workers, trainer.cpp:431-434) rounded up to a multiple of n_shards x rounds; shard g is a
+ * contiguous range of whole chunks, each chunk trained with its reference streams. The replicas are
+ * averaged (fw2v_average + exchange) every ~average_words trained words per shard (0: at the end of
+ * every epoch only) and after every epoch; lr_at counts the words of every shard (trainer.cpp:
+ * 479-487: exact at each average, extrapolated between them). Replicas must start equal (same seed).
+ * Deterministic contexts are rejected (FW2V_ERR_UNSUPPORTED). report: this process's totals,
+ * kernel_seconds summed over rounds of the max over its GPUs. */
+int fw2v_train_corpus_multi(fw2v_ctx* const* ctxs, int32_t n, int32_t shard0, int32_t n_shards,
+                            const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids,
+                            uint64_t average_words, fw2v_exchange_fn exchange, void* exchange_user,
+                            fw2v_observer_fn observer, void* observer_user, fw2v_epoch_fn on_epoch, void* epoch_user,
+                            fw2v_report* report);
 
 /* Host batcher primitives (exposed for tests; same contracts as the
  * reference functions cited). */

@@ -8,6 +8,9 @@ from .fw2v import (  # noqa: F401
     TrainConfig,
     Trainer,
     analytic_traffic,
+    average,
+    nccl_unique_id,
+    train_corpus_multi,
     assemble_batch,
     device_count,
     keep_probs,

@@ -3,6 +3,10 @@
 #pragma once
 
 #include <cstdint>
+#ifdef __CUDACC__
+#include <atomic>
+#include <cuda_runtime.h>
+#endif
 
 namespace fw2v {
 
@@ -50,6 +54,14 @@ constexpr int32_t kFlagNoRing = 32;       // K1s: ring rows stored straight back
 constexpr int32_t kFlagInvalShift = 8;    // bits 8..11: otherwise one warp per block drops the SM's L1 every
                                           // 2^k windows (bounded staleness for Zipf-hot rows; 0 = never)
 
+// Replicas of one matrix for the peer-memory average (fw2v_average): the same
+// |V| x stride buffer on each of n members (device pointers, P2P-accessible).
+constexpr int kMaxPeers = 16;
+struct PeerSet {
+    float* ptr[kMaxPeers];
+    int32_t n;
+};
+
 // Device-side instrumented access counters, in the reference's units
 // (whole-vector accesses, traffic.hpp:19-40).
 struct DevCounters {
@@ -64,5 +76,23 @@ struct DevCounters {
 };
 
 enum ReuseMode : int32_t { kLifetime = 0, kWindow = 1, kNone = 2, kWindowSnapshot = 3 };
+
+#ifdef __CUDACC__
+// Raises a kernel's dynamic shared-memory limit to `bytes` on the CURRENT
+// device. The attribute is per device, so the "already set" record is one bit
+// per device ordinal (contexts on several GPUs in one process each get it).
+// `mask` is the caller's per-kernel static.
+inline cudaError_t ensure_dynamic_smem(const void* kern, int bytes, std::atomic<uint64_t>& mask) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? (uint64_t{1} << dev) : 0;
+    if (bit != 0 && (mask.load(std::memory_order_acquire) & bit) != 0) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && bit != 0) mask.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+#endif
 
 } // namespace fw2v

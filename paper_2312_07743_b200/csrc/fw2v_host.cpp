@@ -54,6 +54,15 @@ bool k1s_supported(int lanes, int vec, int n_neg, int wf, bool lifetime);
 int write_embeddings(const float* rows, int32_t vocab_size, int32_t dim, int64_t row_stride, const char* tokens,
                      const uint64_t* token_offsets, const char* path, int32_t threads, std::string* err);
 void set_last_error(const std::string& msg);
+cudaError_t launch_average_slice(const PeerSet& ps, size_t begin, size_t end, cudaStream_t st);
+// fw2v_nccl.cpp
+struct NcclClique;
+bool nccl_available(std::string* why);
+bool nccl_unique_id(uint8_t out[128], std::string* err);
+std::shared_ptr<NcclClique> nccl_clique_local(const std::vector<int>& devices, std::string* err);
+std::shared_ptr<NcclClique> nccl_clique_rank(int device, const uint8_t id[128], int world, int rank, std::string* err);
+bool nccl_average(NcclClique& c, const std::vector<std::vector<float*>>& buffers, size_t count,
+                  const std::vector<unsigned long long*>& u64, std::string* err);
 } // namespace fw2v
 
 namespace {
@@ -600,6 +609,12 @@ struct fw2v_ctx {
     bool own_model = true;
     std::vector<Lane> lanes;
     uint64_t words_trained = 0;  // schedule counter across calls (EmbeddingModel::words_trained)
+    // Data-parallel replicas (fw2v_average): the NCCL clique this context is a
+    // member of (in-process: every member context; cross-process: this one),
+    // and an 8-byte device word for the global word-count all-reduce.
+    std::shared_ptr<NcclClique> clique;
+    std::vector<fw2v_ctx*> clique_members;
+    unsigned long long* d_words = nullptr;
 
     int32_t k1_flags = 0;
     int64_t inflight_total = 0;  // Hogwild sentences in flight over all streams (0 = unlimited)
@@ -750,6 +765,8 @@ struct fw2v_ctx {
             if (ln.stream2) cudaStreamDestroy(ln.stream2);
             if (ln.copy) cudaStreamDestroy(ln.copy);
         }
+        clique.reset();
+        cudaFree(d_words);
         cudaFree(hot_alloc);
         if (own_model) {
             cudaFree(syn0);
@@ -1073,6 +1090,300 @@ int fw2v_train_sentences(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_senten
     });
 }
 
+} // extern "C"
+
+namespace {
+
+// --------------------------------------------------------------- passes
+// One contiguous range of the corpus with its producer index p: chunk p, batch
+// k uses the reference stream derive(seed, epoch, p, k) (trainer.cpp:442-443).
+struct ChunkSpan {
+    uint64_t p, begin, end;
+};
+
+// State shared by every pass of one run (all GPUs of a multi-GPU run): the
+// global word reservation behind lr_at (trainer.cpp:479-487 counts the words of
+// every worker), the observer's serial counter.
+struct RunShared {
+    std::atomic<uint64_t> reserved{0};
+    uint64_t schedule_total = 1;
+    // Schedule position of local word w: origin + (w - origin) * scale. A process
+    // that trains `scale` times fewer shards than the whole job extrapolates the
+    // global count between exchanges (exact at every average).
+    uint64_t origin = 0, scale = 1;
+    uint64_t position(uint64_t w) const { return origin + (w - origin) * scale; }
+    std::atomic<uint64_t> serial{0};
+    std::mutex obs_mutex;
+    fw2v_observer_fn observer = nullptr;
+    void* observer_user = nullptr;
+};
+
+struct PassOut {
+    fw2v_counters traffic{}, analytic{};
+    uint64_t batch_words = 0, batch_nanos = 0, h2d = 0;
+    double kernel_seconds = 0.0;
+};
+
+void add_counters(fw2v_counters& a, const fw2v_counters& b) {
+    a.context_reads += b.context_reads;
+    a.context_writes += b.context_writes;
+    a.sample_reads += b.sample_reads;
+    a.sample_writes += b.sample_writes;
+    a.ring_hits += b.ring_hits;
+    a.words += b.words;
+    a.sentences += b.sentences;
+}
+
+// Trains ctx x over `spans` (the producer loop of train(), trainer.cpp:429-503):
+// `producers()` batching threads pull whole spans from a shared counter,
+// assemble sub-batches into pinned slots, copy H2D on the lane's copy stream and
+// launch on the lane's kernel streams. Hogwild hot-row replicas are broadcast
+// before and averaged after the pass. Returns after every kernel finished.
+void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan>& spans, int epoch, RunShared& sh,
+              PassOut* out) {
+    FW2V_CK(cudaSetDevice(x->cfg.device));
+    const fw2v_config& cfg = x->cfg;
+    const int NS = static_cast<int>(spans.size());
+    const int P = std::max(1, std::min(x->producers(), NS));  // batching threads = CUDA streams
+    uint64_t cap_w = 1, cap_s = 1, chunk = 1;
+    for (const ChunkSpan& c : spans) {
+        uint64_t w, sn;
+        capacity_for(corpus, c.begin, c.end, cfg.batch_sentences, &w, &sn);
+        cap_w = std::max(cap_w, w);
+        cap_s = std::max(cap_s, sn);
+        chunk = std::max(chunk, c.end - c.begin);
+    }
+    x->ensure_lanes(P, cap_w, cap_s);
+    // Sub-batches of ~256-511 sentences (equal parts of a chunk; enough to keep
+    // the device full across the streams), never above S.
+    static const uint64_t sub_target = [] {
+        const char* e = std::getenv("FW2V_SUB_TARGET");  // experiments
+        return e ? std::max<uint64_t>(1, static_cast<uint64_t>(std::atoll(e))) : uint64_t{256};
+    }();
+    const uint64_t parts = std::max<uint64_t>(1, chunk / sub_target);
+    const uint64_t sub = x->deterministic ? cfg.batch_sentences
+                                          : std::min<uint64_t>(cfg.batch_sentences, (chunk + parts - 1) / parts);
+    static const uint64_t first_sub_env = [] {
+        const char* e = std::getenv("FW2V_FIRST_SUB");  // experiments
+        return e ? static_cast<uint64_t>(std::atoll(e)) : uint64_t{64};
+    }();
+    const uint64_t first_sub = x->deterministic ? 0 : first_sub_env;
+    const int KS = x->kernel_streams();  // kernel streams per lane
+    const Sampler sp = x->sampler();
+    const int n_neg = cfg.negatives;
+    const bool hot = !x->deterministic && x->hot_k > 0;
+
+    struct Events {
+        cudaEvent_t synced = nullptr, t0 = nullptr, t1 = nullptr;
+        std::vector<cudaEvent_t> join;
+        ~Events() {
+            for (cudaEvent_t e : {synced, t0, t1})
+                if (e) cudaEventDestroy(e);
+            for (cudaEvent_t e : join) cudaEventDestroy(e);
+        }
+    } ev;
+    FW2V_CK(cudaEventCreateWithFlags(&ev.synced, cudaEventDisableTiming));
+    FW2V_CK(cudaEventCreate(&ev.t0));
+    FW2V_CK(cudaEventCreate(&ev.t1));
+    ev.join.resize(static_cast<size_t>(2 * P), nullptr);
+    for (auto& e : ev.join) FW2V_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaStream_t s0 = x->lanes[0].stream;
+    // Counters cleared and hot replicas broadcast on lane 0's stream; every
+    // kernel stream starts after them.
+    FW2V_CK(cudaEventRecord(ev.t0, s0));
+    for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), s0));
+    if (hot) x->hot_sync(false, s0);
+    FW2V_CK(cudaEventRecord(ev.synced, s0));
+    for (int p = 0; p < P; ++p) {
+        if (p > 0) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, ev.synced, 0));
+        if (KS > 1) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream2, ev.synced, 0));
+    }
+    // FW2V_TRACE=1: per sub-batch host and device timeline on stderr (diagnostics).
+    struct TraceRec {
+        int p;
+        double t0, t1, t2;
+        cudaEvent_t k0, k1;
+        uint64_t words;
+    };
+    static const bool trace = std::getenv("FW2V_TRACE") != nullptr;
+    std::vector<std::vector<TraceRec>> tr(static_cast<size_t>(P));
+    std::vector<uint64_t> an_acc(static_cast<size_t>(P) * 5, 0);
+    std::vector<std::string> errors(static_cast<size_t>(P));
+    std::atomic<uint64_t> batch_words{0}, batch_nanos{0}, h2d{0};
+    const double t0 = wall_seconds();
+    std::vector<std::thread> threads;
+    std::atomic<int> next_span{0};
+    for (int th = 0; th < P; ++th) {
+        threads.emplace_back([&, th] {
+            try {
+                FW2V_CK(cudaSetDevice(cfg.device));
+                Lane& ln = x->lanes[static_cast<size_t>(th)];
+                double cpu = 0.0;
+                uint64_t wsum = 0;
+                uint64_t* an = &an_acc[static_cast<size_t>(th) * 5];
+                int which = 0;
+                for (int si = next_span.fetch_add(1); si < NS; si = next_span.fetch_add(1)) {
+                    const ChunkSpan& cs_ = spans[static_cast<size_t>(si)];
+                    const uint64_t end = cs_.end;
+                    uint64_t cursor = cs_.begin;
+                    // Batch k (reference stream derive(seed, epoch, p, k), S kept
+                    // sentences) is shipped in sub-batches of `sub` sentences drawn
+                    // from the same stream in the same order, so the kernels of one
+                    // sub-batch overlap the host assembly of the next.
+                    Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), cs_.p, 0);
+                    uint64_t k = 0, left = cfg.batch_sentences;
+                    while (cursor < end) {
+                        if (left == 0) {
+                            ++k;
+                            left = cfg.batch_sentences;
+                            rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), cs_.p, k);
+                        }
+                        Slot& sl = ln.slot[which];
+                        if (sl.in_flight) FW2V_CK(cudaEventSynchronize(sl.h2d_done));
+                        const double c0 = thread_cpu_seconds();
+                        const double w0 = trace ? wall_seconds() : 0.0;
+                        uint64_t words = 0;
+                        const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
+                        // A short first sub-batch per thread gets the device busy early.
+                        const uint64_t want = std::min(left, which == 0 && wsum == 0 && first_sub > 0 ? std::min<uint64_t>(sub, first_sub) : sub);
+                        const uint64_t kept = assemble(corpus, cursor, end, want, sp, rng, bo, &words);
+                        left -= kept;
+                        // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
+                        const uint64_t base = sh.reserved.fetch_add(words);
+                        for (uint64_t q = 0; q < kept; ++q) sl.h_alpha[q] = lr_at(sh.position(base + sl.h_off[q]), sh.schedule_total, cfg.alpha0);
+                        cpu += thread_cpu_seconds() - c0;
+                        wsum += words;
+                        if (kept == 0) continue;
+                        for (uint64_t q = 0; q < kept; ++q) {
+                            uint64_t t[5];
+                            analytic(sl.h_off[q + 1] - sl.h_off[q], x->wf, n_neg, cfg.reuse_mode, t);
+                            for (int z = 0; z < 5; ++z) an[z] += t[z];
+                        }
+                        if (sh.observer) {
+                            const uint64_t s0_ = sh.serial.fetch_add(kept);
+                            std::lock_guard<std::mutex> lk(sh.obs_mutex);
+                            for (uint64_t q = 0; q < kept; ++q)
+                                for (uint32_t i = 0; i < sl.h_off[q + 1] - sl.h_off[q]; ++i) sh.observer(sh.observer_user, s0_ + q, i);
+                        }
+                        // H2D on the lane's copy stream once the kernel that last read
+                        // this slot's device buffers is done; the kernel waits for the copy.
+                        cudaStream_t st = which == 1 && KS > 1 ? ln.stream2 : ln.stream, cs = ln.copy;
+                        if (sl.in_flight) FW2V_CK(cudaStreamWaitEvent(cs, sl.used, 0));
+                        FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, cs));
+                        if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, cs));
+                        FW2V_CK(cudaMemcpyAsync(sl.d_off, sl.h_off, 4 * (kept + 1), cudaMemcpyHostToDevice, cs));
+                        FW2V_CK(cudaMemcpyAsync(sl.d_alpha, sl.h_alpha, 4 * kept, cudaMemcpyHostToDevice, cs));
+                        FW2V_CK(cudaEventRecord(sl.h2d_done, cs));
+                        FW2V_CK(cudaStreamWaitEvent(st, sl.h2d_done, 0));
+                        sl.in_flight = true;
+                        h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
+                        const BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
+                        TraceRec rec{};
+                        if (trace) {
+                            rec = TraceRec{th, w0 - t0, 0.0, 0.0, nullptr, nullptr, words};
+                            rec.t1 = wall_seconds() - t0;
+                            FW2V_CK(cudaEventCreate(&rec.k0));
+                            FW2V_CK(cudaEventCreate(&rec.k1));
+                            FW2V_CK(cudaEventRecord(rec.k0, st));
+                        }
+                        FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, KS * P));
+                        FW2V_CK(cudaEventRecord(sl.used, st));
+                        if (trace) {
+                            FW2V_CK(cudaEventRecord(rec.k1, st));
+                            rec.t2 = wall_seconds() - t0;
+                            tr[static_cast<size_t>(th)].push_back(rec);
+                        }
+                        which ^= 1;
+                    }
+                }
+                batch_words.fetch_add(wsum);
+                batch_nanos.fetch_add(static_cast<uint64_t>(cpu * 1e9));
+            } catch (const Failure& f) {
+                errors[static_cast<size_t>(th)] = f.msg;
+            }
+        });
+    }
+    for (auto& t : threads) t.join();
+    for (const auto& e : errors)
+        if (!e.empty()) {
+            for (int p = 0; p < P; ++p) {  // drain before the caller frees anything
+                cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream);
+                cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream2);
+            }
+            fail(FW2V_ERR_CUDA, e);
+        }
+    // Join every kernel stream on lane 0's stream, fold the replicas back; the
+    // pass ends there (t1: device span of the pass = kernel_seconds).
+    for (int p = 0; p < P; ++p) {
+        Lane& ln = x->lanes[static_cast<size_t>(p)];
+        FW2V_CK(cudaEventRecord(ev.join[static_cast<size_t>(2 * p)], ln.stream));
+        FW2V_CK(cudaStreamWaitEvent(s0, ev.join[static_cast<size_t>(2 * p)], 0));
+        FW2V_CK(cudaEventRecord(ev.join[static_cast<size_t>(2 * p + 1)], ln.stream2));
+        FW2V_CK(cudaStreamWaitEvent(s0, ev.join[static_cast<size_t>(2 * p + 1)], 0));
+    }
+    if (hot) x->hot_sync(true, s0);
+    FW2V_CK(cudaEventRecord(ev.t1, s0));
+    FW2V_CK(cudaEventSynchronize(ev.t1));
+    float ms = 0.0f;
+    FW2V_CK(cudaEventElapsedTime(&ms, ev.t0, ev.t1));
+    if (trace) {
+        std::fprintf(stderr, "[fw2v trace] epoch %d wall %.3f ms (host: asm start/end, launch; device: kernel start/end ms)\n",
+                     epoch, 1e3 * (wall_seconds() - t0));
+        for (auto& lane_tr : tr)
+            for (TraceRec& r : lane_tr) {
+                float a = 0.0f, b = 0.0f;
+                cudaEventElapsedTime(&a, ev.t0, r.k0);
+                cudaEventElapsedTime(&b, ev.t0, r.k1);
+                std::fprintf(stderr, "[fw2v trace] p%02d words %7llu host %.3f %.3f %.3f dev %.3f %.3f\n", r.p,
+                             static_cast<unsigned long long>(r.words), 1e3 * r.t0, 1e3 * r.t1, 1e3 * r.t2, a, b);
+                cudaEventDestroy(r.k0);
+                cudaEventDestroy(r.k1);
+            }
+    }
+    PassOut o;
+    o.kernel_seconds = 1e-3 * ms;
+    for (int p = 0; p < P; ++p) {
+        DevCounters h{};
+        FW2V_CK(cudaMemcpy(&h, x->lanes[static_cast<size_t>(p)].d_ctr, sizeof(h), cudaMemcpyDeviceToHost));
+        add_counters(o.traffic, fw2v_counters{h.context_reads, h.context_writes, h.sample_reads, h.sample_writes,
+                                              h.ring_hits, h.words, h.sentences});
+        const uint64_t* an = &an_acc[static_cast<size_t>(p) * 5];
+        add_counters(o.analytic, fw2v_counters{an[0], an[1], an[2], an[3], an[4], 0, 0});
+    }
+    o.analytic.words = o.traffic.words;
+    o.analytic.sentences = o.traffic.sentences;
+    o.batch_words = batch_words.load();
+    o.batch_nanos = batch_nanos.load();
+    o.h2d = h2d.load();
+    x->words_trained += o.traffic.words;
+    *out = o;
+}
+
+// The reference's producer partition: `nc` contiguous chunks of ceil(n/nc)
+// sentences (trainer.cpp:431-434), chunk p keeping its index for the streams.
+std::vector<ChunkSpan> chunk_spans(uint64_t n_sentences, int nc) {
+    std::vector<ChunkSpan> v;
+    const uint64_t chunk = (n_sentences + nc - 1) / std::max(nc, 1);
+    for (int p = 0; p < nc; ++p) {
+        const uint64_t b = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
+        v.push_back(ChunkSpan{static_cast<uint64_t>(p), b, std::min(n_sentences, b + chunk)});
+    }
+    return v;
+}
+
+void accumulate(fw2v_report& rep, const PassOut& o) {
+    add_counters(rep.traffic, o.traffic);
+    add_counters(rep.analytic, o.analytic);
+    rep.words_trained += o.traffic.words;
+    rep.sentences_trained += o.traffic.sentences;
+    rep.kernel_seconds += o.kernel_seconds;
+    rep.h2d_bytes += o.h2d;
+}
+
+} // namespace
+
+extern "C" {
+
 int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids,
                       fw2v_observer_fn observer, void* observer_user, fw2v_epoch_fn on_epoch,
                       void* epoch_user, fw2v_report* report) {
@@ -1080,250 +1391,306 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
         FW2V_CK(cudaSetDevice(x->cfg.device));
         const fw2v_config& cfg = x->cfg;
         const CorpusView corpus{offsets, ids, n_sentences};
-        const int P = x->producers();  // batching threads = CUDA streams
-        const int NC = x->chunks();
-        const uint64_t chunk = (n_sentences + NC - 1) / std::max(NC, 1);  // trainer.cpp:431-434
-        uint64_t cap_w = 1, cap_s = 1;
-        for (int p = 0; p < NC; ++p) {
-            const uint64_t b = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
-            const uint64_t e = std::min(n_sentences, b + chunk);
-            uint64_t w, s;
-            capacity_for(corpus, b, e, cfg.batch_sentences, &w, &s);
-            cap_w = std::max(cap_w, w);
-            cap_s = std::max(cap_s, s);
-        }
-        x->ensure_lanes(P, cap_w, cap_s);
-        // Sub-batches of ~256-511 sentences (equal parts of a chunk; enough to keep
-        // the device full across the streams), never above S.
-        static const uint64_t sub_target = [] {
-            const char* e = std::getenv("FW2V_SUB_TARGET");  // experiments
-            return e ? std::max<uint64_t>(1, static_cast<uint64_t>(std::atoll(e))) : uint64_t{256};
-        }();
-        const uint64_t parts = std::max<uint64_t>(1, chunk / sub_target);
-        const uint64_t sub = x->deterministic ? cfg.batch_sentences
-                                              : std::min<uint64_t>(cfg.batch_sentences, (chunk + parts - 1) / parts);
-        static const uint64_t first_sub_env = [] {
-            const char* e = std::getenv("FW2V_FIRST_SUB");  // experiments
-            return e ? static_cast<uint64_t>(std::atoll(e)) : uint64_t{64};
-        }();
-        const uint64_t first_sub = x->deterministic ? 0 : first_sub_env;
-        const int KS = x->kernel_streams();  // kernel streams per lane
-        const uint64_t schedule_total =
+        const std::vector<ChunkSpan> spans = chunk_spans(n_sentences, x->chunks());
+        RunShared sh;
+        sh.schedule_total =
             cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
-        const Sampler sp = x->sampler();
-        const int n_neg = cfg.negatives;
-
+        sh.observer = observer;
+        sh.observer_user = observer_user;
         fw2v_report rep{};
         rep.vocab_size = static_cast<uint64_t>(x->vocab);
-        std::atomic<uint64_t> serial_ctr{0};
-        std::atomic<uint64_t> batch_words{0};
-        std::atomic<uint64_t> batch_nanos{0};
-        std::atomic<uint64_t> h2d{0};
-        std::mutex obs_mutex;
+        uint64_t bw = 0, bn = 0;
         const double run_start = wall_seconds();
-
-        cudaEvent_t synced;
-        FW2V_CK(cudaEventCreateWithFlags(&synced, cudaEventDisableTiming));
-        struct EvGuard {
-            cudaEvent_t e;
-            ~EvGuard() { cudaEventDestroy(e); }
-        } ev_guard{synced};
         for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
-            // Counters cleared and hot replicas broadcast on lane 0's stream; every
-            // kernel stream starts after them.
-            for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), x->lanes[0].stream));
-            if (!x->deterministic && x->hot_k > 0) x->hot_sync(false, x->lanes[0].stream);
-            FW2V_CK(cudaEventRecord(synced, x->lanes[0].stream));
-            for (int p = 0; p < P; ++p) {
-                if (p > 0) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, synced, 0));
-                if (KS > 1) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream2, synced, 0));
-            }
-            std::atomic<uint64_t> reserved{x->words_trained};
-            // FW2V_TRACE=1: per sub-batch host and device timeline on stderr (diagnostics).
-            struct TraceRec {
-                int p;
-                double t0, t1, t2;
-                cudaEvent_t k0, k1;
-                uint64_t words;
-            };
-            static const bool trace = std::getenv("FW2V_TRACE") != nullptr;
-            std::vector<std::vector<TraceRec>> tr(static_cast<size_t>(P));
-            cudaEvent_t ev0 = nullptr;
-            if (trace) {
-                FW2V_CK(cudaEventCreate(&ev0));
-                FW2V_CK(cudaEventRecord(ev0, x->lanes[0].stream));
-                FW2V_CK(cudaEventSynchronize(ev0));
-            }
-            std::vector<uint64_t> an_acc(static_cast<size_t>(P) * 5, 0);
-            std::vector<std::string> errors(static_cast<size_t>(P));
+            sh.reserved.store(x->words_trained);
             const double t0 = wall_seconds();
-            std::vector<std::thread> threads;
-            std::atomic<int> next_chunk{0};
-            for (int th = 0; th < P; ++th) {
-                threads.emplace_back([&, th] {
-                    try {
-                        FW2V_CK(cudaSetDevice(cfg.device));
-                        Lane& ln = x->lanes[static_cast<size_t>(th)];
-                        double cpu = 0.0;
-                        uint64_t wsum = 0;
-                        uint64_t* an = &an_acc[static_cast<size_t>(th) * 5];
-                        int which = 0;
-                        for (int p = next_chunk.fetch_add(1); p < NC; p = next_chunk.fetch_add(1)) {
-                        const uint64_t begin = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
-                        const uint64_t end = std::min(n_sentences, begin + chunk);
-                        uint64_t cursor = begin;
-                        // Batch k (reference stream derive(seed, epoch, p, k), S kept
-                        // sentences) is shipped in sub-batches of `sub` sentences drawn
-                        // from the same stream in the same order, so the kernels of one
-                        // sub-batch overlap the host assembly of the next.
-                        Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), 0);
-                        uint64_t k = 0, left = cfg.batch_sentences;
-                        while (cursor < end) {
-                            if (left == 0) {
-                                ++k;
-                                left = cfg.batch_sentences;
-                                rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), k);
-                            }
-                            Slot& sl = ln.slot[which];
-                            if (sl.in_flight) FW2V_CK(cudaEventSynchronize(sl.h2d_done));
-                            const double c0 = thread_cpu_seconds();
-                            const double w0 = trace ? wall_seconds() : 0.0;
-                            uint64_t words = 0;
-                            const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
-                            // A short first sub-batch per thread gets the device busy early.
-                            const uint64_t want = std::min(left, which == 0 && wsum == 0 && first_sub > 0 ? std::min<uint64_t>(sub, first_sub) : sub);
-                            const uint64_t kept = assemble(corpus, cursor, end, want, sp, rng, bo, &words);
-                            left -= kept;
-                            // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
-                            const uint64_t base = reserved.fetch_add(words);
-                            for (uint64_t q = 0; q < kept; ++q) sl.h_alpha[q] = lr_at(base + sl.h_off[q], schedule_total, cfg.alpha0);
-                            cpu += thread_cpu_seconds() - c0;
-                            wsum += words;
-                            if (kept == 0) continue;
-                            for (uint64_t q = 0; q < kept; ++q) {
-                                uint64_t t[5];
-                                analytic(sl.h_off[q + 1] - sl.h_off[q], x->wf, n_neg, cfg.reuse_mode, t);
-                                for (int z = 0; z < 5; ++z) an[z] += t[z];
-                            }
-                            if (observer) {
-                                const uint64_t s0 = serial_ctr.fetch_add(kept);
-                                std::lock_guard<std::mutex> lk(obs_mutex);
-                                for (uint64_t q = 0; q < kept; ++q)
-                                    for (uint32_t i = 0; i < sl.h_off[q + 1] - sl.h_off[q]; ++i) observer(observer_user, s0 + q, i);
-                            }
-                            // H2D on the lane's copy stream once the kernel that last read
-                            // this slot's device buffers is done; the kernel waits for the copy.
-                            cudaStream_t st = which == 1 && KS > 1 ? ln.stream2 : ln.stream, cs = ln.copy;
-                            if (sl.in_flight) FW2V_CK(cudaStreamWaitEvent(cs, sl.used, 0));
-                            FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, cs));
-                            if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, cs));
-                            FW2V_CK(cudaMemcpyAsync(sl.d_off, sl.h_off, 4 * (kept + 1), cudaMemcpyHostToDevice, cs));
-                            FW2V_CK(cudaMemcpyAsync(sl.d_alpha, sl.h_alpha, 4 * kept, cudaMemcpyHostToDevice, cs));
-                            FW2V_CK(cudaEventRecord(sl.h2d_done, cs));
-                            FW2V_CK(cudaStreamWaitEvent(st, sl.h2d_done, 0));
-                            sl.in_flight = true;
-                            h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
-                            const BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
-                            TraceRec rec{};
-                            if (trace) {
-                                rec = TraceRec{th, w0 - t0, 0.0, 0.0, nullptr, nullptr, words};
-                                rec.t1 = wall_seconds() - t0;
-                                FW2V_CK(cudaEventCreate(&rec.k0));
-                                FW2V_CK(cudaEventCreate(&rec.k1));
-                                FW2V_CK(cudaEventRecord(rec.k0, st));
-                            }
-                            FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, KS * P));
-                            FW2V_CK(cudaEventRecord(sl.used, st));
-                            if (trace) {
-                                FW2V_CK(cudaEventRecord(rec.k1, st));
-                                rec.t2 = wall_seconds() - t0;
-                                tr[static_cast<size_t>(th)].push_back(rec);
-                            }
-                            which ^= 1;
-                        }
-                        }  // chunks
-                        batch_words.fetch_add(wsum);
-                        batch_nanos.fetch_add(static_cast<uint64_t>(cpu * 1e9));
-                    } catch (const Failure& f) {
-                        errors[static_cast<size_t>(th)] = f.msg;
-                    }
-                });
-            }
-            for (auto& t : threads) t.join();
-            for (int p = 0; p < P; ++p) {
-                FW2V_CK(cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream));
-                FW2V_CK(cudaStreamSynchronize(x->lanes[static_cast<size_t>(p)].stream2));
-            }
-            if (!x->deterministic && x->hot_k > 0) {
-                x->hot_sync(true, x->lanes[0].stream);
-                FW2V_CK(cudaStreamSynchronize(x->lanes[0].stream));
-            }
-            if (trace) {
-                std::fprintf(stderr, "[fw2v trace] epoch %d wall %.3f ms (host: asm start/end, launch; device: kernel start/end ms)\n",
-                             epoch, 1e3 * (wall_seconds() - t0));
-                for (auto& lane_tr : tr)
-                    for (TraceRec& r : lane_tr) {
-                        float a = 0.0f, b = 0.0f;
-                        cudaEventElapsedTime(&a, ev0, r.k0);
-                        cudaEventElapsedTime(&b, ev0, r.k1);
-                        std::fprintf(stderr, "[fw2v trace] p%02d words %7llu host %.3f %.3f %.3f dev %.3f %.3f\n", r.p,
-                                     static_cast<unsigned long long>(r.words), 1e3 * r.t0, 1e3 * r.t1, 1e3 * r.t2, a, b);
-                        cudaEventDestroy(r.k0);
-                        cudaEventDestroy(r.k1);
-                    }
-                cudaEventDestroy(ev0);
-            }
-            for (const auto& e : errors)
-                if (!e.empty()) fail(FW2V_ERR_CUDA, e);
+            PassOut o;
+            run_pass(x, corpus, spans, epoch, sh, &o);
             const double secs = wall_seconds() - t0;
-            uint64_t epoch_words = 0;
-            for (int p = 0; p < P; ++p) {
-                DevCounters h{};
-                FW2V_CK(cudaMemcpy(&h, x->lanes[static_cast<size_t>(p)].d_ctr, sizeof(h), cudaMemcpyDeviceToHost));
-                rep.traffic.context_reads += h.context_reads;
-                rep.traffic.context_writes += h.context_writes;
-                rep.traffic.sample_reads += h.sample_reads;
-                rep.traffic.sample_writes += h.sample_writes;
-                rep.traffic.ring_hits += h.ring_hits;
-                rep.traffic.words += h.words;
-                rep.traffic.sentences += h.sentences;
-                epoch_words += h.words;
-                rep.sentences_trained += h.sentences;
-                const uint64_t* an = &an_acc[static_cast<size_t>(p) * 5];
-                rep.analytic.context_reads += an[0];
-                rep.analytic.context_writes += an[1];
-                rep.analytic.sample_reads += an[2];
-                rep.analytic.sample_writes += an[3];
-                rep.analytic.ring_hits += an[4];
-            }
-            x->words_trained += epoch_words;
-            rep.words_trained += epoch_words;
+            accumulate(rep, o);
+            bw += o.batch_words;
+            bn += o.batch_nanos;
             rep.n_epochs = epoch + 1;
             if (on_epoch) {
+                const uint64_t ew = o.traffic.words;
+                fw2v_epoch_stats st{epoch, ew, secs, secs > 0 ? static_cast<double>(ew) / secs : 0.0};
+                on_epoch(epoch_user, &st);
+            }
+        }
+        rep.wall_seconds = wall_seconds() - run_start;
+        rep.batching_words_per_sec = bn > 0 ? static_cast<double>(bw) * 1e9 / static_cast<double>(bn) : 0.0;
+        if (report) *report = rep;
+    });
+}
+
+} // extern "C"
+
+namespace {
+
+// Replica average over `n` contexts (see fw2v_average). local_words[i] (may be
+// null) are the words each member trained since the last exchange; *global
+// (may be null) receives their sum over every member of every process.
+void average_impl(fw2v_ctx* const* ctxs, int n, const uint64_t* local_words, uint64_t* global) {
+    if (n < 1) fail(FW2V_ERR_BAD_ARGUMENT, "need at least one context");
+    if (n > kMaxPeers) fail(FW2V_ERR_UNSUPPORTED, "at most 16 contexts per process");
+    fw2v_ctx* x0 = ctxs[0];
+    std::vector<int> devices;
+    bool distinct = true;
+    uint64_t local_sum = 0;
+    for (int i = 0; i < n; ++i) {
+        fw2v_ctx* x = ctxs[i];
+        if (x->vocab != x0->vocab || x->stride != x0->stride || x->cfg.dim != x0->cfg.dim)
+            fail(FW2V_ERR_BAD_ARGUMENT, "replicas differ in vocabulary or row stride");
+        if (std::find(devices.begin(), devices.end(), x->cfg.device) != devices.end()) distinct = false;
+        devices.push_back(x->cfg.device);
+        if (local_words) local_sum += local_words[i];
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        FW2V_CK(cudaDeviceSynchronize());  // training must be quiesced; cheap when it is
+    }
+    const size_t count = static_cast<size_t>(x0->vocab) * static_cast<size_t>(x0->stride);
+    const bool cross = x0->clique != nullptr && x0->clique_members.size() == 1 && n == 1;
+    static const bool force_peer = [] {
+        const char* e = std::getenv("FW2V_AVERAGE");
+        return e != nullptr && std::strcmp(e, "peer") == 0;
+    }();
+    std::string err;
+    if (cross || (n > 1 && distinct && !force_peer && nccl_available(nullptr))) {
+        if (!cross && (x0->clique == nullptr || x0->clique_members != std::vector<fw2v_ctx*>(ctxs, ctxs + n))) {
+            auto c = nccl_clique_local(devices, &err);
+            if (!c) fail(FW2V_ERR_CUDA, err);
+            for (int i = 0; i < n; ++i) {
+                ctxs[i]->clique = c;
+                ctxs[i]->clique_members.assign(ctxs, ctxs + n);
+            }
+        }
+        std::vector<std::vector<float*>> bufs;
+        std::vector<unsigned long long*> words;
+        for (int i = 0; i < n; ++i) {
+            fw2v_ctx* x = ctxs[i];
+            bufs.push_back({x->syn0, x->syn1});
+            if (cross && global != nullptr) {
+                FW2V_CK(cudaSetDevice(x->cfg.device));
+                if (x->d_words == nullptr) FW2V_CK(cudaMalloc(&x->d_words, sizeof(unsigned long long)));
+                const unsigned long long w = local_sum;
+                FW2V_CK(cudaMemcpy(x->d_words, &w, sizeof(w), cudaMemcpyHostToDevice));
+                words.push_back(x->d_words);
+            }
+        }
+        if (!nccl_average(*x0->clique, bufs, count, words, &err)) fail(FW2V_ERR_CUDA, err);
+        if (global != nullptr) {
+            if (cross) {
+                unsigned long long w = 0;
+                FW2V_CK(cudaSetDevice(x0->cfg.device));
+                FW2V_CK(cudaMemcpy(&w, x0->d_words, sizeof(w), cudaMemcpyDeviceToHost));
+                *global = w;
+            } else {
+                *global = local_sum;
+            }
+        }
+        return;
+    }
+    if (global != nullptr) *global = local_sum;
+    if (n == 1) return;
+    // Peer-memory kernel: member g averages its slice of every replica.
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            if (devices[i] == devices[j]) continue;
+            int can = 0;
+            FW2V_CK(cudaDeviceCanAccessPeer(&can, devices[i], devices[j]));
+            if (!can) fail(FW2V_ERR_UNSUPPORTED, "no P2P access between the replicas' devices and no NCCL");
+            FW2V_CK(cudaSetDevice(devices[i]));
+            cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else FW2V_CK(e);
+        }
+    for (int m = 0; m < 2; ++m) {
+        PeerSet ps{};
+        ps.n = n;
+        for (int i = 0; i < n; ++i) ps.ptr[i] = m == 0 ? ctxs[i]->syn0 : ctxs[i]->syn1;
+        const size_t per = ((count + n - 1) / n + 3) & ~size_t(3);
+        for (int g = 0; g < n; ++g) {
+            FW2V_CK(cudaSetDevice(devices[g]));
+            const size_t b = std::min(count, per * g), e = std::min(count, b + per);
+            FW2V_CK(launch_average_slice(ps, b, e, nullptr));
+        }
+    }
+    for (int g = 0; g < n; ++g) {
+        FW2V_CK(cudaSetDevice(devices[g]));
+        FW2V_CK(cudaDeviceSynchronize());
+    }
+}
+
+// The job's chunk partition for data-parallel runs: the reference's `workers`
+// chunks (trainer.cpp:431-434) rounded up to a multiple of n_shards * rounds,
+// so every shard is a contiguous range of whole chunks and every round of a
+// shard the same number of them.
+struct DpPlan {
+    int total_chunks = 1, per_shard = 1, per_round = 1, rounds = 1;
+};
+
+DpPlan dp_plan(const fw2v_ctx& x, const CorpusView& c, int n_shards, uint64_t average_words) {
+    DpPlan d;
+    // Estimated trained words per shard and epoch (expected_epoch_words scaled
+    // by the shard's share of the tokens).
+    const double shard_words = static_cast<double>(expected_epoch_words(x)) / n_shards;
+    d.rounds = average_words > 0
+                   ? static_cast<int>(std::max(1.0, std::floor(shard_words / static_cast<double>(average_words) + 0.5)))
+                   : 1;
+    const int unit = n_shards * d.rounds;
+    d.total_chunks = ((std::max(x.chunks(), n_shards) + unit - 1) / unit) * unit;
+    d.per_shard = d.total_chunks / n_shards;
+    d.per_round = d.per_shard / d.rounds;
+    (void)c;
+    return d;
+}
+
+std::vector<ChunkSpan> round_spans(const std::vector<ChunkSpan>& all, const DpPlan& d, int shard, int round) {
+    const int b = shard * d.per_shard + round * d.per_round;
+    return std::vector<ChunkSpan>(all.begin() + b, all.begin() + b + d.per_round);
+}
+
+} // namespace
+
+extern "C" {
+
+int fw2v_average(fw2v_ctx* const* ctxs, int32_t n) {
+    return guarded([&] { average_impl(ctxs, n, nullptr, nullptr); });
+}
+
+int fw2v_nccl_unique_id(uint8_t out[128]) {
+    return guarded([&] {
+        std::string err;
+        if (!nccl_unique_id(out, &err)) fail(FW2V_ERR_UNSUPPORTED, err);
+    });
+}
+
+int fw2v_comm_init_rank(fw2v_ctx* x, const uint8_t id[128], int32_t world, int32_t rank) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(FW2V_ERR_BAD_ARGUMENT, "bad rank / world");
+        std::string err;
+        auto c = nccl_clique_rank(x->cfg.device, id, world, rank, &err);
+        if (!c) fail(FW2V_ERR_CUDA, err);
+        x->clique = c;
+        x->clique_members = {x};
+    });
+}
+
+int fw2v_train_corpus_multi(fw2v_ctx* const* ctxs, int32_t n, int32_t shard0, int32_t n_shards,
+                            const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids,
+                            uint64_t average_words, fw2v_exchange_fn exchange, void* exchange_user,
+                            fw2v_observer_fn observer, void* observer_user, fw2v_epoch_fn on_epoch, void* epoch_user,
+                            fw2v_report* report) {
+    return guarded([&] {
+        if (n < 1 || n_shards < n || shard0 < 0 || shard0 + n > n_shards)
+            fail(FW2V_ERR_BAD_ARGUMENT, "shards shard0 .. shard0+n-1 must lie in 0 .. n_shards-1");
+        fw2v_ctx* x0 = ctxs[0];
+        for (int i = 0; i < n; ++i) {
+            if (ctxs[i]->deterministic)
+                fail(FW2V_ERR_UNSUPPORTED, "deterministic mode is single-GPU (serial reference order)");
+            if (ctxs[i]->vocab != x0->vocab || ctxs[i]->cfg.epochs != x0->cfg.epochs)
+                fail(FW2V_ERR_BAD_ARGUMENT, "replicas differ in vocabulary or epochs");
+        }
+        const bool cross = n_shards > n;
+        if (cross && exchange == nullptr && (n != 1 || x0->clique == nullptr || x0->clique_members.size() != 1))
+            fail(FW2V_ERR_BAD_ARGUMENT, "other processes hold shards: pass an exchange callback or fw2v_comm_init_rank");
+        const fw2v_config& cfg = x0->cfg;
+        const CorpusView corpus{offsets, ids, n_sentences};
+        const DpPlan d = dp_plan(*x0, corpus, n_shards, average_words);
+        const std::vector<ChunkSpan> all = chunk_spans(n_sentences, d.total_chunks);
+        RunShared sh;
+        sh.schedule_total =
+            cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x0)) : 1;
+        sh.observer = observer;
+        sh.observer_user = observer_user;
+        uint64_t global_words = 0;
+        for (int i = 0; i < n; ++i) global_words = std::max(global_words, ctxs[i]->words_trained);
+        sh.scale = static_cast<uint64_t>(n_shards / n);
+        fw2v_report rep{};
+        rep.vocab_size = static_cast<uint64_t>(x0->vocab);
+        uint64_t bw = 0, bn = 0;
+        const double run_start = wall_seconds();
+        for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
+            const double t0 = wall_seconds();
+            uint64_t epoch_words = 0;
+            for (int r = 0; r < d.rounds; ++r) {
+                sh.origin = global_words;
+                sh.reserved.store(global_words);
+                std::vector<PassOut> outs(static_cast<size_t>(n));
+                std::vector<std::string> errs(static_cast<size_t>(n));
+                std::vector<int> codes(static_cast<size_t>(n), FW2V_OK);
+                std::vector<std::thread> th;
+                for (int i = 0; i < n; ++i)
+                    th.emplace_back([&, i] {
+                        try {
+                            run_pass(ctxs[i], corpus, round_spans(all, d, shard0 + i, r), epoch, sh,
+                                     &outs[static_cast<size_t>(i)]);
+                        } catch (const Failure& f) {
+                            codes[static_cast<size_t>(i)] = f.code;
+                            errs[static_cast<size_t>(i)] = f.msg;
+                        }
+                    });
+                for (auto& t : th) t.join();
+                for (int i = 0; i < n; ++i)
+                    if (codes[static_cast<size_t>(i)] != FW2V_OK) fail(codes[static_cast<size_t>(i)], errs[static_cast<size_t>(i)]);
+                std::vector<uint64_t> lw(static_cast<size_t>(n));
+                double ks = 0.0;
+                for (int i = 0; i < n; ++i) {
+                    const PassOut& o = outs[static_cast<size_t>(i)];
+                    lw[static_cast<size_t>(i)] = o.traffic.words;
+                    accumulate(rep, o);
+                    rep.kernel_seconds -= o.kernel_seconds;  // max over GPUs, added below
+                    ks = std::max(ks, o.kernel_seconds);
+                    bw += o.batch_words;
+                    bn += o.batch_nanos;
+                    epoch_words += o.traffic.words;
+                }
+                rep.kernel_seconds += ks;
+                // Exchange: replicas <- their mean over every shard; the global word
+                // count is exact again (lr_at's position, trainer.cpp:479-487).
+                uint64_t g = 0;
+                average_impl(ctxs, n, lw.data(), &g);
+                if (exchange != nullptr) {
+                    uint64_t gg = g;
+                    const int rc = exchange(exchange_user, g, &gg);
+                    if (rc != FW2V_OK) fail(rc, "exchange callback failed");
+                    g = gg;
+                }
+                global_words += g;
+            }
+            for (int i = 0; i < n; ++i) ctxs[i]->words_trained = global_words;
+            rep.n_epochs = epoch + 1;
+            if (on_epoch) {
+                const double secs = wall_seconds() - t0;
                 fw2v_epoch_stats st{epoch, epoch_words, secs, secs > 0 ? static_cast<double>(epoch_words) / secs : 0.0};
                 on_epoch(epoch_user, &st);
             }
         }
-        rep.analytic.words = rep.traffic.words;
-        rep.analytic.sentences = rep.traffic.sentences;
         rep.wall_seconds = wall_seconds() - run_start;
-        const uint64_t ns = batch_nanos.load();
-        rep.batching_words_per_sec = ns > 0 ? static_cast<double>(batch_words.load()) * 1e9 / static_cast<double>(ns) : 0.0;
-        rep.h2d_bytes = h2d.load();
+        rep.batching_words_per_sec = bn > 0 ? static_cast<double>(bw) * 1e9 / static_cast<double>(bn) : 0.0;
         if (report) *report = rep;
     });
 }
 
 int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids,
                     int32_t epoch, fw2v_plan** out) {
+    const int nc = x->chunks();
+    return fw2v_plan_chunks(x, offsets, n_sentences, ids, epoch, nc, 0, nc, x->words_trained, 1, out);
+}
+
+int fw2v_plan_chunks(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, const int32_t* ids, int32_t epoch,
+                     int32_t n_chunks, int32_t chunk_begin, int32_t chunk_end, uint64_t words_base,
+                     int32_t words_scale, fw2v_plan** out) {
     *out = nullptr;
     return guarded([&] {
+        if (n_chunks < 1 || chunk_begin < 0 || chunk_end > n_chunks || chunk_begin > chunk_end || words_scale < 1)
+            fail(FW2V_ERR_BAD_ARGUMENT, "chunk range must lie in 0 .. n_chunks, words_scale >= 1");
         FW2V_CK(cudaSetDevice(x->cfg.device));
         const fw2v_config& cfg = x->cfg;
         const CorpusView corpus{offsets, ids, n_sentences};
         const int P = x->producers();  // streams the plan's launches are spread over
-        const int NC = x->chunks();
-        const uint64_t chunk = (n_sentences + NC - 1) / std::max(NC, 1);
+        const std::vector<ChunkSpan> all = chunk_spans(n_sentences, n_chunks);
+        const std::vector<ChunkSpan> spans(all.begin() + chunk_begin, all.begin() + chunk_end);
+        const int NC = static_cast<int>(spans.size());
         const uint64_t schedule_total =
             cfg.epochs > 0 ? std::max<uint64_t>(1, static_cast<uint64_t>(cfg.epochs) * expected_epoch_words(*x)) : 1;
         const Sampler sp = x->sampler();
@@ -1334,22 +1701,24 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
             std::vector<float> alpha;
         };
         std::vector<std::vector<HostBatch>> host(static_cast<size_t>(NC));
-        std::atomic<uint64_t> reserved{x->words_trained};
+        std::atomic<uint64_t> reserved{words_base};
+        auto position = [&](uint64_t w) { return words_base + (w - words_base) * static_cast<uint64_t>(words_scale); };
         std::vector<std::thread> threads;
         std::atomic<int> next_chunk{0};
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         for (unsigned th = 0; th < std::min<unsigned>(hw, static_cast<unsigned>(NC)); ++th) {
             threads.emplace_back([&] {
-              for (int p = next_chunk.fetch_add(1); p < NC; p = next_chunk.fetch_add(1)) {
-                const uint64_t begin = std::min(n_sentences, static_cast<uint64_t>(p) * chunk);
-                const uint64_t end = std::min(n_sentences, begin + chunk);
+              for (int si = next_chunk.fetch_add(1); si < NC; si = next_chunk.fetch_add(1)) {
+                const uint64_t p = spans[static_cast<size_t>(si)].p;
+                const uint64_t begin = spans[static_cast<size_t>(si)].begin;
+                const uint64_t end = spans[static_cast<size_t>(si)].end;
                 uint64_t cap_w, cap_s;
                 capacity_for(corpus, begin, std::max(begin, end), cfg.batch_sentences, &cap_w, &cap_s);
                 std::vector<int32_t> bi(cap_w), bn(cap_w * std::max(n_neg, 1));
                 std::vector<uint32_t> bo(cap_s + 1);
                 uint64_t cursor = begin;
                 for (uint64_t k = 0; cursor < end; ++k) {
-                    Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), k);
+                    Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), p, k);
                     uint64_t words = 0;
                     const uint64_t kept = assemble(corpus, cursor, end, cfg.batch_sentences, sp, rng,
                                                    BatchOut{bi.data(), bo.data(), bn.data(), cap_w, cap_s}, &words);
@@ -1361,8 +1730,8 @@ int fw2v_plan_epoch(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences, 
                     hb.off.assign(bo.begin(), bo.begin() + static_cast<ptrdiff_t>(kept + 1));
                     const uint64_t base = reserved.fetch_add(words);
                     hb.alpha.resize(kept);
-                    for (uint64_t q = 0; q < kept; ++q) hb.alpha[q] = lr_at(base + bo[q], schedule_total, cfg.alpha0);
-                    host[static_cast<size_t>(p)].push_back(std::move(hb));
+                    for (uint64_t q = 0; q < kept; ++q) hb.alpha[q] = lr_at(position(base + bo[q]), schedule_total, cfg.alpha0);
+                    host[static_cast<size_t>(si)].push_back(std::move(hb));
                 }
               }
             });

@@ -594,12 +594,12 @@ cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf,
     if (wf < 1 || 2 * wf + 1 > kMaxRing) return cudaErrorInvalidValue;
     if (b.n_sentences == 0) return cudaSuccess;
     const size_t smem = k2_smem_bytes(m.dim, wf, n_neg);
-    static thread_local size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    // The attribute is per device: always raise it for sizes above 48 KB (K2 runs
+    // one launch per batch, so the driver call is negligible).
+    if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k2_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        configured = smem;
     }
     const int grid = serial ? 1 : b.n_sentences;
     k2_exact<<<grid, 32, smem, st>>>(m, b, n_neg, wf, mode, serial ? 1 : 0, ctr);
@@ -635,6 +635,32 @@ cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st) {
     const int blocks = (n + 255) / 256;
     if (average) k_hot_average<<<blocks, 256, 0, st>>>(m);
     else k_hot_broadcast<<<blocks, 256, 0, st>>>(m);
+    return cudaGetLastError();
+}
+
+// Replica average over peer memory (fw2v_average without NCCL: contexts that
+// share a device, or FW2V_AVERAGE=peer). Launched once per member g on g's own
+// device: member g owns elements [begin, end) and reads that slice of every
+// replica (NVLink P2P loads for remote ones), writes the mean back into every
+// replica. Slices are disjoint, so the members' launches need no ordering
+// among themselves; the host quiesces training before and joins after.
+// begin, end: multiples of 4 (row strides are), replicas 16-byte aligned.
+__global__ void k_average_slice(PeerSet ps, size_t begin, size_t end) {
+    const float inv = 1.0f / static_cast<float>(ps.n);
+    const size_t nth = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t x = begin / 4 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; x < end / 4; x += nth) {
+        float4 s = reinterpret_cast<const float4*>(ps.ptr[0])[x];
+        for (int r = 1; r < ps.n; ++r) {
+            const float4 v = reinterpret_cast<const float4*>(ps.ptr[r])[x];
+            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+        }
+        s.x *= inv; s.y *= inv; s.z *= inv; s.w *= inv;
+        for (int r = 0; r < ps.n; ++r) reinterpret_cast<float4*>(ps.ptr[r])[x] = s;
+    }
+}
+cudaError_t launch_average_slice(const PeerSet& ps, size_t begin, size_t end, cudaStream_t st) {
+    if (end <= begin || ps.n < 1) return cudaSuccess;
+    k_average_slice<<<148 * 4, 256, 0, st>>>(ps, begin, end);
     return cudaGetLastError();
 }
 

@@ -334,7 +334,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
 
     const int32_t* __restrict__ ids = b.ids + beg;
     const int32_t* __restrict__ negs = b.negs + static_cast<size_t>(beg) * n_neg;
-    // Row offsets use the compile-time stride (host checks |V| * stride < 2^31).
+    // Row offsets: 64-bit products of the compile-time stride (|V| * stride may exceed 2^31).
     float* __restrict__ syn0 = m.syn0 + sub * SL::CW;
     float* __restrict__ syn1 = m.syn1 + sub * SL::CW;
     // Output row of sample s >= 0: hot rows go to this sentence's replica.
@@ -368,13 +368,13 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
     int tok[NCTX];
     float2 tgt[H2];
     int ttok = L > 0 ? __ldg(ids) : -1;
-    if (ttok >= 0) SL::load(tgt, syn0 + ttok * STRIDE); else vzero2(tgt);
+    if (ttok >= 0) SL::load(tgt, syn0 + static_cast<int64_t>(ttok) * STRIDE); else vzero2(tgt);
     if (delta_wb) SL::store_shared(ring, tgt);  // position 0 -> slot 0
 #pragma unroll
     for (int r = 0; r < NCTX; ++r) {
         const int p = r - WF + 1;
         tok[r] = (r >= WF && p < L) ? __ldg(ids + p) : -1;
-        if (tok[r] >= 0) SL::load(ctx[r], syn0 + tok[r] * STRIDE); else vzero2(ctx[r]);
+        if (tok[r] >= 0) SL::load(ctx[r], syn0 + static_cast<int64_t>(tok[r]) * STRIDE); else vzero2(ctx[r]);
         if (delta_wb && r >= WF) SL::store_shared(ring + p * STRIDE, ctx[r]);  // p < C
     }
     unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
@@ -485,7 +485,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
         }
         const int inc_tok = tok_ahead;
         float2 inc[H2];
-        SL::load_early(inc, syn0 + max(inc_tok, 0) * STRIDE);
+        SL::load_early(inc, syn0 + static_cast<int64_t>(max(inc_tok, 0)) * STRIDE);
         const int last = max(L - 1, 0);
         const int tok_raw = ldg_early(ids + min(q_in + 1, last));
         if constexpr (!MULTI) {
@@ -794,13 +794,13 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
         if (etok >= 0) {
             const int p = i - WF;
             if (!RING) {
-                SL::store(syn0 + etok * STRIDE, ctx[0]);
+                SL::store(syn0 + static_cast<int64_t>(etok) * STRIDE, ctx[0]);
             } else if (delta_wb) {
-                SL::red_delta(syn0 + etok * STRIDE, ctx[0], ring + (p % C) * STRIDE);
+                SL::red_delta(syn0 + static_cast<int64_t>(etok) * STRIDE, ctx[0], ring + (p % C) * STRIDE);
             } else if (p >= tail) {
                 SL::store_shared(ring + (p % C) * STRIDE, ctx[0]);
             } else {
-                SL::store(syn0 + etok * STRIDE, ctx[0]);
+                SL::store(syn0 + static_cast<int64_t>(etok) * STRIDE, ctx[0]);
             }
             if (inc_tok == etok) vcopy2(inc, ctx[0]);
         }
@@ -841,16 +841,16 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
     if (!RING) {
 #pragma unroll
         for (int r = 0; r < NCTX; ++r)
-            if (tok[r] >= 0) SL::store(syn0 + tok[r] * STRIDE, ctx[r]);
-        if (ttok >= 0) SL::store(syn0 + ttok * STRIDE, tgt);
+            if (tok[r] >= 0) SL::store(syn0 + static_cast<int64_t>(tok[r]) * STRIDE, ctx[r]);
+        if (ttok >= 0) SL::store(syn0 + static_cast<int64_t>(ttok) * STRIDE, tgt);
     } else if (delta_wb) {
         // Deltas commute: no ordering to preserve.
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) {
             const int p = r < WF ? i_end - WF + r : i_end + 1 + (r - WF);
-            if (tok[r] >= 0) SL::red_delta(syn0 + tok[r] * STRIDE, ctx[r], ring + (p % C) * STRIDE);
+            if (tok[r] >= 0) SL::red_delta(syn0 + static_cast<int64_t>(tok[r]) * STRIDE, ctx[r], ring + (p % C) * STRIDE);
         }
-        if (ttok >= 0) SL::red_delta(syn0 + ttok * STRIDE, tgt, ring + (i_end % C) * STRIDE);
+        if (ttok >= 0) SL::red_delta(syn0 + static_cast<int64_t>(ttok) * STRIDE, tgt, ring + (i_end % C) * STRIDE);
     } else {
 #pragma unroll
         for (int r = 0; r < NCTX; ++r) {
@@ -865,7 +865,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
             if (p < L) {
                 float2 v[H2];
                 SL::load_shared(v, ring + s * STRIDE);
-                SL::store(syn0 + __ldg(ids + p) * STRIDE, v);
+                SL::store(syn0 + static_cast<int64_t>(__ldg(ids + p)) * STRIDE, v);
             }
         }
     }
@@ -897,12 +897,9 @@ cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, 
     using SMx = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == kMultiChunk && !LIFETIME>;
     constexpr int bytes = SMx::kBlockBytes;
     auto* kern = k1s_snapshot<LANES, VEC, WF, NC, MODE, FAST, RING, LIFETIME>;
-    static bool configured = false;  // benign race: idempotent attribute set
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};  // one bit per device ordinal
+    if (cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), bytes, configured); e != cudaSuccess)
+        return e;
     constexpr int threads = SMx::THREADS;
     if (resident != nullptr) return resident_sentences(kern, bytes, threads, threads / LANES, resident);
     if (blocks == 0) return cudaSuccess;

@@ -12,6 +12,7 @@
 //   fw2v_report  -> RunReport / EpochStats, observer and on_epoch trampolines.
 // workers == 1 selects the serial bit-exact engine (reference: "workers == 1
 // is fully deterministic", trainer.hpp:115-118); workers > 1 the Hogwild path.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -98,26 +99,49 @@ TrainResult train(const Corpus& corpus, const TrainConfig& raw_config, TrainObse
     c.ignore_delimiters = cfg.ignore_delimiters ? 1 : 0;
     c.device = env_int("FW2V_DEVICE", 0);
     c.deterministic = env_int("FW2V_DETERMINISTIC", -1);
-    c.sampler = env_int("FW2V_SAMPLER", FW2V_SAMPLER_REFERENCE);
+    // Hogwild runs draw negatives from the unigram^0.75 alias table (north_star's
+    // throughput sampler; same stream positions, so the same sentences are kept);
+    // deterministic runs always use the reference slot table (fw2v_ctx::sampler).
+    c.sampler = env_int("FW2V_SAMPLER", FW2V_SAMPLER_ALIAS);
     c.fast_sigmoid = env_int("FW2V_FAST_SIGMOID", 1);
     c.k1_lanes = env_int("FW2V_K1_LANES", 0);
     c.streams = env_int("FW2V_STREAMS", 0);
     c.l1_refresh_log2 = env_int("FW2V_L1_REFRESH_LOG2", c.l1_refresh_log2);
     c.delta_writeback = env_int("FW2V_DELTA_WRITEBACK", c.delta_writeback);
     c.max_inflight = env_int("FW2V_MAX_INFLIGHT", c.max_inflight);
-    c.hot_rows = env_int("FW2V_HOT_ROWS", c.hot_rows);
+    // Hot-row replicas change the update rule of the most frequent output rows
+    // (each replica sees 1/R of the sentences; merged as their mean), so the
+    // drop-in keeps plain Hogwild unless FW2V_HOT_ROWS asks for them.
+    c.hot_rows = env_int("FW2V_HOT_ROWS", 0);
     c.hot_replicas = env_int("FW2V_HOT_REPLICAS", c.hot_replicas);
 
     std::vector<uint64_t> counts(static_cast<size_t>(vocab.size()));
     for (int32_t w = 0; w < vocab.size(); ++w) counts[static_cast<size_t>(w)] = vocab.entry(w).count;
 
-    fw2v_ctx* ctx = nullptr;
-    int rc = fw2v_create(&c, counts.data(), vocab.size(), &ctx);
-    if (rc != FW2V_OK) raise_status(rc);
+    // FW2V_GPUS = G > 1 (Hogwild only): data-parallel replicas on devices
+    // FW2V_DEVICE .. FW2V_DEVICE+G-1, contiguous corpus shards, replicas averaged
+    // every FW2V_AVERAGE_WORDS trained words per GPU (NCCL over NVLink) and after
+    // every epoch (fw2v_train_corpus_multi). All replicas start from the same
+    // init_model(seed).
+    const int gpus = std::max(1, env_int("FW2V_GPUS", 1));
+    const bool serial = c.deterministic == 1 || (c.deterministic < 0 && c.workers == 1);
+    const int n_ctx = serial ? 1 : gpus;
     struct Guard {
-        fw2v_ctx* p;
-        ~Guard() { fw2v_destroy(p); }
-    } guard{ctx};
+        std::vector<fw2v_ctx*> p;
+        ~Guard() {
+            for (fw2v_ctx* x : p) fw2v_destroy(x);
+        }
+    } guard;
+    int rc = FW2V_OK;
+    for (int g = 0; g < n_ctx; ++g) {
+        fw2v_config cg = c;
+        cg.device = c.device + g;
+        fw2v_ctx* x = nullptr;
+        rc = fw2v_create(&cg, counts.data(), vocab.size(), &x);
+        if (rc != FW2V_OK) raise_status(rc);
+        guard.p.push_back(x);
+    }
+    fw2v_ctx* ctx = guard.p[0];
 
     std::vector<uint64_t> offsets(corpus.sentences.size() + 1, 0);
     for (size_t s = 0; s < corpus.sentences.size(); ++s) offsets[s + 1] = offsets[s] + corpus.sentences[s].length();
@@ -128,9 +152,16 @@ TrainResult train(const Corpus& corpus, const TrainConfig& raw_config, TrainObse
 
     Callbacks cb{observer, &on_epoch, {}};
     fw2v_report rep{};
-    rc = fw2v_train_corpus(ctx, offsets.data(), corpus.sentences.size(), ids.data(),
-                           observer ? observer_tramp : nullptr, &cb, epoch_tramp, &cb,
-                           &rep);
+    if (n_ctx == 1) {
+        rc = fw2v_train_corpus(ctx, offsets.data(), corpus.sentences.size(), ids.data(),
+                               observer ? observer_tramp : nullptr, &cb, epoch_tramp, &cb, &rep);
+    } else {
+        const char* aw = std::getenv("FW2V_AVERAGE_WORDS");
+        const uint64_t average_words = (aw && *aw) ? std::strtoull(aw, nullptr, 10) : uint64_t{25000000};
+        rc = fw2v_train_corpus_multi(guard.p.data(), n_ctx, 0, n_ctx, offsets.data(), corpus.sentences.size(),
+                                     ids.data(), average_words, nullptr, nullptr, observer ? observer_tramp : nullptr,
+                                     &cb, epoch_tramp, &cb, &rep);
+    }
     if (rc != FW2V_OK) raise_status(rc);
 
     TrainResult result;

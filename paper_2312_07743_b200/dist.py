@@ -1,16 +1,22 @@
 """Multi-GPU plumbing for the FULL-W2V trainer: one process per GPU.
 
 The path shards naturally: sentences are independent Hogwild
-units, so each rank trains its own replica of syn0/syn1neg on a contiguous
-sentence range (the reference's producer chunking, trainer.cpp:431-434) and
-the only exchange is a periodic replica average — one in-place NCCL
-all-reduce with ReduceOp.AVG over both matrices, held in one flat tensor so a
-single collective covers the whole model (NVLS on NVSwitch systems).
-The learning-rate schedule counts the GLOBAL trained words (all ranks).
+units, so each GPU trains its own replica of syn0/syn1neg on a contiguous shard
+of the corpus (whole chunks of the reference's producer partition,
+trainer.cpp:431-434) and the only exchange is a periodic replica average. The
+product path for that is native: ``fw2v_train_corpus_multi`` (include/fw2v.h)
+runs the rounds, keeps the learning-rate schedule on the GLOBAL word count
+(trainer.cpp:479-487) and averages with NCCL (``ncclAllReduce`` / ``ncclAvg``,
+in-process over ``ncclCommInitAll`` or across processes after
+``fw2v_comm_init_rank``).
+
+This module holds the Python side of a multi-process job: sharding arithmetic
+and ``TorchExchange``, the exchange callback for process groups NCCL cannot
+serve (gloo on CPU, or several ranks sharing one GPU in tests): it averages
+model tensors attached to the trainer (``Trainer.attach_model``) with
+``torch.distributed`` and sums the word counts.
 """
 from __future__ import annotations
-
-from dataclasses import dataclass
 
 
 def shard_bounds(n_sentences: int, rank: int, world: int) -> tuple[int, int]:
@@ -22,22 +28,22 @@ def shard_bounds(n_sentences: int, rank: int, world: int) -> tuple[int, int]:
     return begin, min(n_sentences, begin + chunk)
 
 
-@dataclass
-class AveragePolicy:
-    """Average the replicas every `period_words` words trained per rank."""
-
-    period_words: int
-
-    def due(self, words_since_last: int) -> bool:
-        return words_since_last >= self.period_words
+def dp_chunks(workers: int, n_shards: int, rounds: int) -> tuple[int, int, int]:
+    """The data-parallel chunk partition fw2v_train_corpus_multi uses: the
+    reference's `workers` chunks rounded up to a multiple of n_shards x rounds.
+    Returns (total chunks, chunks per shard, chunks per round)."""
+    if workers < 1 or n_shards < 1 or rounds < 1:
+        raise ValueError("workers, n_shards and rounds must be >= 1")
+    unit = n_shards * rounds
+    total = ((max(workers, n_shards) + unit - 1) // unit) * unit
+    return total, total // n_shards, total // n_shards // rounds
 
 
 class ReplicaAverager:
     """In-place replica averaging of a flat model tensor over a process group.
 
-    `model` holds syn0 and syn1neg back to back (2 x |V| x stride fp32); on the
-    NCCL backend this is one ncclAllReduce(ncclAvg) over NVLink. Works on any
-    torch.distributed backend (gloo on CPU for tests).
+    `model` holds syn0 and syn1neg back to back (2 x |V| x stride fp32). On the
+    NCCL backend this is one all-reduce (AVG); gloo sums and divides.
     """
 
     def __init__(self, model, group=None):
@@ -51,8 +57,13 @@ class ReplicaAverager:
     def average(self):
         dist = self.dist
         if dist.get_backend(self.group) == "gloo" or not hasattr(dist.ReduceOp, "AVG"):
-            dist.all_reduce(self.model, op=dist.ReduceOp.SUM, group=self.group)
-            self.model.div_(dist.get_world_size(self.group))
+            if self.model.is_cuda and dist.get_backend(self.group) == "gloo":
+                host = self.model.cpu()
+                dist.all_reduce(host, op=dist.ReduceOp.SUM, group=self.group)
+                self.model.copy_(host.div_(dist.get_world_size(self.group)))
+            else:
+                dist.all_reduce(self.model, op=dist.ReduceOp.SUM, group=self.group)
+                self.model.div_(dist.get_world_size(self.group))
         else:
             dist.all_reduce(self.model, op=dist.ReduceOp.AVG, group=self.group)
         self.rounds += 1
@@ -68,3 +79,24 @@ def global_words(local_words: int, group=None) -> int:
         t = t.cuda()
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return int(t.item())
+
+
+class TorchExchange:
+    """Exchange callback for ``train_corpus_multi(..., exchange=...)``: averages
+    the attached replica tensor over the process group and returns the global
+    word count. Called by the native trainer after this process's kernels
+    finished (so the model is quiescent)."""
+
+    def __init__(self, model, group=None):
+        self.averager = ReplicaAverager(model, group)
+        self.group = group
+        self.calls = 0
+
+    def __call__(self, local_words: int) -> int:
+        import torch
+
+        if self.averager.model.is_cuda:
+            torch.cuda.synchronize(self.averager.model.device)
+        self.averager.average()
+        self.calls += 1
+        return global_words(local_words, self.group)

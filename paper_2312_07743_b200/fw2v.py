@@ -45,7 +45,8 @@ EXPORTED = [
     "fw2v_plan_run", "fw2v_plan_destroy", "fw2v_keep_probs", "fw2v_table_build",
     "fw2v_assemble_batch", "fw2v_lr_at", "fw2v_analytic_traffic", "fw2v_corpus_synth_zipf",
     "fw2v_corpus_view", "fw2v_corpus_free", "fw2v_write_embeddings", "fw2v_save_model",
-    "fw2v_nearest_neighbors", "fw2v_eval_analogy", "fw2v_alias_draws",
+    "fw2v_nearest_neighbors", "fw2v_eval_analogy", "fw2v_alias_draws", "fw2v_plan_chunks",
+    "fw2v_average", "fw2v_nccl_unique_id", "fw2v_comm_init_rank", "fw2v_train_corpus_multi",
 ]
 
 
@@ -94,6 +95,7 @@ class CReport(C.Structure):
 
 
 OBSERVER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_uint64)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64))
 EPOCH_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(CEpoch))
 
 
@@ -158,6 +160,7 @@ class Report:
     analytic: tuple
     h2d_bytes: int
     epochs: list = field(default_factory=list)
+    kernel_seconds: float = 0.0
 
 
 _lib = None
@@ -432,8 +435,24 @@ class Trainer:
         rep = CReport()
         _check(lib().fw2v_train_corpus(self._h, _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1),
                                        _p(ids, C.c_int32), cb_obs, None, cb_ep, None, C.byref(rep)))
-        return Report(rep.words_trained, rep.sentences_trained, rep.wall_seconds, rep.batching_words_per_sec,
-                      rep.traffic.as_tuple(), rep.analytic.as_tuple(), rep.h2d_bytes, epochs)
+        return _report(rep, epochs)
+
+    def plan_chunks(self, corpus: Corpus, n_chunks: int, chunk_begin: int, chunk_end: int, epoch: int = 0,
+                    words_base: int = 0, words_scale: int = 1) -> "Plan":
+        """Device-resident batches of chunks [chunk_begin, chunk_end) of an n_chunks partition
+        (one shard / one averaging round of a data-parallel job; fw2v_plan_chunks)."""
+        offsets = np.ascontiguousarray(corpus.offsets, np.uint64)
+        ids = np.ascontiguousarray(corpus.ids, np.int32)
+        h = C.c_void_p()
+        _check(lib().fw2v_plan_chunks(self._h, _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1),
+                                      _p(ids, C.c_int32), epoch, n_chunks, chunk_begin, chunk_end,
+                                      C.c_uint64(words_base), words_scale, C.byref(h)))
+        return Plan(self, h)
+
+    def comm_init_rank(self, unique_id: bytes, world: int, rank: int):
+        """Joins a cross-process NCCL communicator (fw2v_comm_init_rank)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(lib().fw2v_comm_init_rank(self._h, buf, world, rank))
 
     def plan_epoch(self, corpus: Corpus, epoch: int = 0) -> "Plan":
         offsets = np.ascontiguousarray(corpus.offsets, np.uint64)
@@ -442,6 +461,61 @@ class Trainer:
         _check(lib().fw2v_plan_epoch(self._h, _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1),
                                      _p(ids, C.c_int32), epoch, C.byref(h)))
         return Plan(self, h)
+
+
+def _report(rep, epochs) -> Report:
+    return Report(rep.words_trained, rep.sentences_trained, rep.wall_seconds, rep.batching_words_per_sec,
+                  rep.traffic.as_tuple(), rep.analytic.as_tuple(), rep.h2d_bytes, epochs, rep.kernel_seconds)
+
+
+def _handles(trainers):
+    arr = (C.c_void_p * len(trainers))(*[t._h for t in trainers])
+    return arr
+
+
+def average(trainers):
+    """Replica average over trainers (fw2v_average): NCCL across devices, peer kernel otherwise."""
+    _check(lib().fw2v_average(_handles(trainers), len(trainers)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().fw2v_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def train_corpus_multi(trainers, corpus: Corpus, average_words: int = 0, shard0: int = 0, n_shards: int = 0,
+                       exchange=None, on_epoch=None) -> Report:
+    """Data-parallel training (fw2v_train_corpus_multi): trainer i trains shard shard0+i of n_shards
+    (default: len(trainers)); exchange(local_words) -> global_words averages across processes."""
+    offsets = np.ascontiguousarray(corpus.offsets, np.uint64)
+    ids = np.ascontiguousarray(corpus.ids, np.int32)
+    epochs = []
+
+    def _ep(_u, st):
+        e = st.contents
+        epochs.append(dict(epoch=e.epoch, words=e.words, seconds=e.seconds, words_per_sec=e.words_per_sec))
+        if on_epoch:
+            on_epoch(epochs[-1])
+
+    def _ex(_u, local, out):
+        try:
+            out[0] = int(exchange(int(local)))
+            return 0
+        except Exception:  # noqa: BLE001 - reported through the status code
+            import traceback
+
+            traceback.print_exc()
+            return ERR_BAD_ARGUMENT
+
+    cb_ep = EPOCH_FN(_ep)
+    cb_ex = EXCHANGE_FN(_ex) if exchange else EXCHANGE_FN()
+    rep = CReport()
+    _check(lib().fw2v_train_corpus_multi(_handles(trainers), len(trainers), shard0, n_shards or len(trainers),
+                                         _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1), _p(ids, C.c_int32),
+                                         C.c_uint64(average_words), cb_ex, None, OBSERVER_FN(), None, cb_ep, None,
+                                         C.byref(rep)))
+    return _report(rep, epochs)
 
 
 class Plan:

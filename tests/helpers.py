@@ -31,7 +31,7 @@ def fixed_negatives(n_words, n_neg, vocab, seed):
     return rng.integers(0, vocab, n_words * n_neg).astype(np.int32)
 
 
-def sgns_loss(inp, out, offsets, ids, negs, wf, n_neg, max_pairs=200_000, seed=0):
+def sgns_loss(inp, out, offsets, ids, negs, wf, n_neg, max_pairs=200_000, seed=0, split=None):
     """Mean SGNS objective over (context, target, negatives) triples of a fixed
     sample (SURVEY.md §7 hard part 7): -log s(c.t) - sum_n log s(-c.n), with c
     from the input matrix and t, n from the output matrix."""
@@ -58,4 +58,9 @@ def sgns_loss(inp, out, offsets, ids, negs, wf, n_neg, max_pairs=200_000, seed=0
     ls = lambda x: -np.logaddexp(0.0, -x)  # noqa: E731  log sigmoid
     pos = ls(np.einsum("ij,ij->i", c, t))
     neg = ls(-np.einsum("ij,ikj->ik", c, n)).sum(axis=1)
-    return float(-(pos + neg).mean())
+    per = -(pos + neg)
+    if split is not None:
+        # (loss over triples whose target id < split, loss over the rest)
+        hot = np.array(trip_t) < split
+        return float(per[hot].mean()), float(per[~hot].mean())
+    return float(per.mean())

@@ -1,5 +1,6 @@
 """Multi-process host logic on CPU (gloo, world_size 2): corpus sharding, the
-replica average, and the global word count behind the lr schedule."""
+data-parallel chunk partition, the replica average, the global word count
+behind the lr schedule, and the exchange callback the native trainer calls."""
 import os
 import socket
 
@@ -9,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2312_07743_b200.dist import AveragePolicy, ReplicaAverager, global_words, shard_bounds
+from paper_2312_07743_b200.dist import ReplicaAverager, TorchExchange, dp_chunks, global_words, shard_bounds
 
 
 def test_shard_bounds_cover_and_match_reference_chunking():
@@ -25,9 +26,20 @@ def test_shard_bounds_cover_and_match_reference_chunking():
         shard_bounds(10, 2, 2)
 
 
-def test_average_policy():
-    p = AveragePolicy(period_words=1000)
-    assert not p.due(999) and p.due(1000)
+def test_dp_chunks_whole_rounds():
+    # workers already a multiple of shards x rounds: the reference's own partition
+    assert dp_chunks(16, 2, 2) == (16, 8, 4)
+    assert dp_chunks(64, 8, 1) == (64, 8, 8)
+    # rounded up so every shard and round holds whole chunks
+    assert dp_chunks(10, 4, 1) == (12, 3, 3)
+    assert dp_chunks(1, 8, 3) == (24, 3, 1)
+    for w in range(1, 40):
+        for s in (1, 2, 3, 8):
+            for r in (1, 2, 5):
+                tot, per_shard, per_round = dp_chunks(w, s, r)
+                assert tot >= max(w, s) and tot % (s * r) == 0 and per_shard * s == tot and per_round * r == per_shard
+    with pytest.raises(ValueError):
+        dp_chunks(0, 1, 1)
 
 
 def _free_port():
@@ -45,7 +57,12 @@ def _worker(rank, world, port, q):
         avg = ReplicaAverager(model)
         avg.average()
         words = global_words(1000 * (rank + 1))
-        q.put((rank, model.mean().item(), float(model.std()), words, avg.rounds))
+        # the exchange callback: replicas differ per element, words per rank
+        rng = np.random.default_rng(rank)
+        m2 = torch.from_numpy(rng.standard_normal((2, 7, 12)).astype(np.float32))
+        ex = TorchExchange(m2)
+        g = ex(123 + rank)
+        q.put((rank, model.mean().item(), float(model.std()), words, avg.rounds, m2.numpy().copy(), g, ex.calls))
     finally:
         dist.destroy_process_group()
 
@@ -57,11 +74,14 @@ def test_replica_average_gloo_world2():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda r: r[0])
     for p in procs:
         p.join(120)
         assert p.exitcode == 0
-    res = sorted(q.get() for _ in range(world))
-    for rank, mean, std, words, rounds in res:
+    want = sum(np.random.default_rng(r).standard_normal((2, 7, 12)).astype(np.float32) for r in range(world)) / world
+    for rank, mean, std, words, rounds, m2, g, calls in res:
         assert mean == pytest.approx(0.5) and std == 0.0
         assert words == 3000 and rounds == 1
-    np.testing.assert_equal(len(res), world)
+        np.testing.assert_allclose(m2, want, rtol=0, atol=1e-6)
+        assert g == 123 + 124 and calls == 1
+    np.testing.assert_array_equal(res[0][5], res[1][5])  # replicas identical after the exchange

@@ -116,14 +116,16 @@ def test_hogwild_quality_d512(reference_run_d512, mode):
     assert recall >= ref_recall - 0.01
 
 
-def test_text8_multi_epoch_stable(ref):
-    """Five Hogwild epochs on the text8-shaped Zipf corpus at d=128 (the bench
-    workload): with the in-flight budget and hot-row replicas the B200 run stays
-    within 2% of the reference's SGNS loss. (Without them, ~3,000 sentences in
-    flight diverge here: loss 3e18.)"""
-    import os
+# The bench's exact configuration (bench.py defaults): alias sampler, 64 chunks
+# on 16 batching threads / streams, L1 refresh every 2^5 windows, ring-less
+# overwrite write-back, fast sigmoid, top-64 output rows as 16 replicas.
+BENCH_KNOBS = dict(workers=64, streams=16, sampler="alias", l1_refresh_log2=5, delta_writeback=2, fast_sigmoid=True,
+                   hot_rows=64, hot_replicas=16, deterministic=0)
 
-    from helpers import sgns_loss
+
+@pytest.fixture(scope="module")
+def text8_reference(ref):
+    import os
 
     c = fw.synth_zipf(**fw.TEXT8_SHAPE)
     cfg = dict(dim=128, window=5, negatives=5, epochs=5, batch_sentences=10000, subsample=1e-4, seed=1)
@@ -131,14 +133,41 @@ def test_text8_multi_epoch_stable(ref):
     negs = np.random.default_rng(5).choice(len(c.counts), 400_000 * 5, p=p / p.sum()).astype(np.int32)
     off = c.offsets[:401].copy()
 
-    def loss(inp, out):
-        return sgns_loss(inp, out, off, c.ids[: int(off[-1])], negs, wf=3, n_neg=5, max_pairs=100_000)
+    def loss(inp, out, split=None):
+        return sgns_loss(inp, out, off, c.ids[: int(off[-1])], negs, wf=3, n_neg=5, max_pairs=100_000, split=split)
 
     rin, rout, _ = ref.train(c.counts, c.offsets, c.ids, RConfig(workers=os.cpu_count() or 8, **cfg))
-    with fw.Trainer(fw.TrainConfig(workers=16, deterministic=0, reuse_mode="window_snapshot", **cfg), c.counts) as t:
+    return c, cfg, loss, rin, rout
+
+
+@pytest.mark.parametrize("mode", ["window_snapshot", "lifetime"])
+def test_text8_multi_epoch_stable(text8_reference, mode):
+    """Five Hogwild epochs on the text8-shaped Zipf corpus at d=128 with the
+    bench's exact knobs (BENCH_KNOBS), both update orders: the B200 run stays
+    within 2% of the reference's SGNS loss. (Without the in-flight budget and
+    replicas, ~3,000 sentences in flight diverge here: loss 3e18.)"""
+    c, cfg, loss, rin, rout = text8_reference
+    with fw.Trainer(fw.TrainConfig(reuse_mode=mode, **cfg, **BENCH_KNOBS), c.counts) as t:
         t.train_corpus(c)
         gin, gout = t.get_model()
     ref_loss, got = loss(rin, rout), loss(gin, gout)
-    print(f"text8 5 epochs: loss {got:.4f} vs ref {ref_loss:.4f}")
+    print(f"text8 5 epochs {mode}: loss {got:.4f} vs ref {ref_loss:.4f}")
     assert np.isfinite(gin).all() and np.isfinite(gout).all()
     assert abs(got - ref_loss) / ref_loss <= 0.02
+
+
+@pytest.mark.parametrize("hot_rows", [64, 0], ids=["replicas", "plain"])
+def test_text8_hot_band_loss(text8_reference, hot_rows):
+    """The loss split by target frequency band: targets among the top-64 output
+    rows (the replicated ones; ~4% of sample reductions) vs the rest, with the
+    replicas on and off. Each band within 2% of the reference's same band."""
+    c, cfg, loss, rin, rout = text8_reference
+    kn = dict(BENCH_KNOBS, hot_rows=hot_rows)
+    with fw.Trainer(fw.TrainConfig(reuse_mode="window_snapshot", **cfg, **kn), c.counts) as t:
+        t.train_corpus(c)
+        gin, gout = t.get_model()
+    (rh, rr), (gh, gr) = loss(rin, rout, split=64), loss(gin, gout, split=64)
+    print(f"text8 hot-band hot_rows={hot_rows}: top-64 targets {gh:.4f} vs ref {rh:.4f} ({100 * (gh / rh - 1):+.2f}%), "
+          f"rest {gr:.4f} vs ref {rr:.4f} ({100 * (gr / rr - 1):+.2f}%)")
+    assert abs(gh - rh) / rh <= 0.02
+    assert abs(gr - rr) / rr <= 0.02
