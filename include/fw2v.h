@@ -90,7 +90,16 @@ typedef struct fw2v_config {
                               broadcast before and averaged after every pass; removes the L2
                               contention and the stale-update pile-up on Zipf-hot rows. 0 = off */
     int32_t hot_replicas;
+    int32_t replica_merge; /* data-parallel rounds (fw2v_train_corpus_multi), per element with b the
+                              replicas' common value at the round start and d_r = v_r - b:
+                              0 mean: mean of the replicas (model averaging; every update scaled by
+                              1/replicas); 1 touched: b + sum d_r / #{r: d_r != 0} (an element only
+                              one shard trained keeps its full update, others get the mean);
+                              2 sum: b + sum d_r (every update applied, like Hogwild with the round as
+                              staleness) */
 } fw2v_config;
+
+enum fw2v_replica_merge { FW2V_MERGE_MEAN = 0, FW2V_MERGE_TOUCHED = 1, FW2V_MERGE_SUM = 2 };
 
 /* ringvec::TrafficCounters (traffic.hpp:19-40) plus totals. */
 typedef struct fw2v_counters {
@@ -215,18 +224,23 @@ int fw2v_average(fw2v_ctx* const* ctxs, int32_t n);
 int fw2v_nccl_unique_id(uint8_t out[128]);
 int fw2v_comm_init_rank(fw2v_ctx* ctx, const uint8_t id[128], int32_t world, int32_t rank);
 
-/* Exchange across processes, called by fw2v_train_corpus_multi at every averaging point after this
- * process's kernels finished and its own contexts were averaged: must average the replicas over
- * all processes in place (e.g. torch.distributed all_reduce of attached model tensors) and set
- * *global_words to the sum of local_words over processes. Returns 0 or an fw2v status. */
-typedef int (*fw2v_exchange_fn)(void* user, uint64_t local_words, uint64_t* global_words);
+/* Exchange across processes, called by fw2v_train_corpus_multi at every merge point after this
+ * process's kernels finished: must SUM each of the n_bufs device buffers (counts[i] fp32 each)
+ * over all processes in place (e.g. torch.distributed all_reduce over __cuda_array_interface__
+ * views) and set *global_words to the sum of local_words over processes. The library turns the
+ * replicas into the summands before (delta / indicator per replica_merge) and the sums into the
+ * merged model after. Returns 0 or an fw2v status. */
+typedef int (*fw2v_exchange_fn)(void* user, float* const* bufs, const uint64_t* counts, int32_t n_bufs,
+                                uint64_t local_words, uint64_t* global_words);
 
 /* Data-parallel training: this call trains shards shard0 .. shard0+n-1 (context i <- shard
  * shard0+i) of an n_shards-shard job (n_shards > n: other processes hold the rest and `exchange`
- * or fw2v_comm_init_rank connects them). The corpus is cut into the reference's producer chunks
+ * or fw2v_comm_init_rank connects them; one context per process then). Replicas are merged per
+ * ctxs[0]'s replica_merge rule (NCCL SUM all-reduce between prep / finish kernels, or one fused
+ * peer-memory kernel when the contexts share a device). The corpus is cut into the reference's producer chunks
  * (cfg.workers, trainer.cpp:431-434) rounded up to a multiple of n_shards x rounds; shard g is a
  * contiguous range of whole chunks, each chunk trained with its reference streams. The replicas are
- * averaged (fw2v_average + exchange) every ~average_words trained words per shard (0: at the end of
+ * merged every ~average_words trained words per shard (0: at the end of
  * every epoch only) and after every epoch; lr_at counts the words of every shard (trainer.cpp:
  * 479-487: exact at each average, extrapolated between them). Replicas must start equal (same seed).
  * Deterministic contexts are rejected (FW2V_ERR_UNSUPPORTED). report: this process's totals,

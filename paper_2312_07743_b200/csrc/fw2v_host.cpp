@@ -61,8 +61,12 @@ bool nccl_available(std::string* why);
 bool nccl_unique_id(uint8_t out[128], std::string* err);
 std::shared_ptr<NcclClique> nccl_clique_local(const std::vector<int>& devices, std::string* err);
 std::shared_ptr<NcclClique> nccl_clique_rank(int device, const uint8_t id[128], int world, int rank, std::string* err);
-bool nccl_average(NcclClique& c, const std::vector<std::vector<float*>>& buffers, size_t count,
-                  const std::vector<unsigned long long*>& u64, std::string* err);
+bool nccl_allreduce(NcclClique& c, const std::vector<std::vector<float*>>& buffers, size_t count,
+                    const std::vector<unsigned long long*>& u64, bool sum, std::string* err);
+cudaError_t launch_merge_slice(const PeerSet& ps, float* base, int rule, size_t begin, size_t end, cudaStream_t st);
+cudaError_t launch_merge_prep(float* v, const float* base, float* cnt, int rule, size_t n, cudaStream_t st);
+cudaError_t launch_merge_finish(float* v, float* base, const float* cnt, int rule, float inv_n, size_t n,
+                                cudaStream_t st);
 } // namespace fw2v
 
 namespace {
@@ -541,6 +545,7 @@ void validate(const fw2v_config& c) {  // validate_config (config.cpp:165-177)
     if (c.sampler < 0 || c.sampler > 1) fail(FW2V_ERR_BAD_CONFIG, "unknown sampler");
     if (c.hot_rows < 0 || c.hot_replicas < 1) fail(FW2V_ERR_BAD_CONFIG, "hot_rows must be >= 0 and hot_replicas >= 1");
     if (c.delta_writeback < 0 || c.delta_writeback > 2) fail(FW2V_ERR_BAD_CONFIG, "delta_writeback must be 0, 1 or 2");
+    if (c.replica_merge < 0 || c.replica_merge > 2) fail(FW2V_ERR_BAD_CONFIG, "replica_merge must be 0, 1 or 2");
 }
 
 void require_device(int device) {
@@ -615,6 +620,11 @@ struct fw2v_ctx {
     std::shared_ptr<NcclClique> clique;
     std::vector<fw2v_ctx*> clique_members;
     unsigned long long* d_words = nullptr;
+    // Replica merge state (fw2v_train_corpus_multi): the round's base model and,
+    // for the touched rule, the changed-element indicators; [syn0 | syn1] each.
+    float* merge_base = nullptr;
+    float* merge_cnt = nullptr;
+    size_t model_floats() const { return static_cast<size_t>(vocab) * static_cast<size_t>(stride); }
 
     int32_t k1_flags = 0;
     int64_t inflight_total = 0;  // Hogwild sentences in flight over all streams (0 = unlimited)
@@ -767,6 +777,8 @@ struct fw2v_ctx {
         }
         clique.reset();
         cudaFree(d_words);
+        cudaFree(merge_base);
+        cudaFree(merge_cnt);
         cudaFree(hot_alloc);
         if (own_model) {
             cudaFree(syn0);
@@ -875,6 +887,7 @@ void fw2v_config_default(fw2v_config* c) {
     c->max_inflight = 0;
     c->hot_rows = 64;
     c->hot_replicas = 16;
+    c->replica_merge = FW2V_MERGE_TOUCHED;
 }
 
 int fw2v_validate_config(const fw2v_config* cfg) {
@@ -1476,7 +1489,7 @@ void average_impl(fw2v_ctx* const* ctxs, int n, const uint64_t* local_words, uin
                 words.push_back(x->d_words);
             }
         }
-        if (!nccl_average(*x0->clique, bufs, count, words, &err)) fail(FW2V_ERR_CUDA, err);
+        if (!nccl_allreduce(*x0->clique, bufs, count, words, false, &err)) fail(FW2V_ERR_CUDA, err);
         if (global != nullptr) {
             if (cross) {
                 unsigned long long w = 0;
@@ -1518,6 +1531,145 @@ void average_impl(fw2v_ctx* const* ctxs, int n, const uint64_t* local_words, uin
         FW2V_CK(cudaSetDevice(devices[g]));
         FW2V_CK(cudaDeviceSynchronize());
     }
+}
+
+// Allocates the merge buffers and makes the base the current model.
+void merge_begin(fw2v_ctx* x, int rule) {
+    if (rule == kMergeMean) return;
+    FW2V_CK(cudaSetDevice(x->cfg.device));
+    const size_t n = x->model_floats();
+    if (x->merge_base == nullptr) FW2V_CK(cudaMalloc(&x->merge_base, 2 * n * sizeof(float)));
+    if (rule == kMergeTouched && x->merge_cnt == nullptr) FW2V_CK(cudaMalloc(&x->merge_cnt, 2 * n * sizeof(float)));
+    FW2V_CK(cudaMemcpy(x->merge_base, x->syn0, n * sizeof(float), cudaMemcpyDeviceToDevice));
+    FW2V_CK(cudaMemcpy(x->merge_base + n, x->syn1, n * sizeof(float), cudaMemcpyDeviceToDevice));
+}
+
+// One merge of the replicas of an n_total-replica job, of which ctxs[0..n) are
+// here (see fw2v_config.replica_merge). Returns the global word count.
+uint64_t merge_impl(fw2v_ctx* const* ctxs, int n, int n_total, int rule, const uint64_t* local_words,
+                    fw2v_exchange_fn exchange, void* user) {
+    uint64_t local_sum = 0;
+    for (int i = 0; i < n; ++i) local_sum += local_words[i];
+    fw2v_ctx* x0 = ctxs[0];
+    const size_t count = x0->model_floats();
+    const bool cross = n_total > n;
+    if (!cross) {
+        if (n == 1) return local_sum;
+        std::vector<int> devices;
+        bool distinct = true;
+        for (int i = 0; i < n; ++i) {
+            if (std::find(devices.begin(), devices.end(), ctxs[i]->cfg.device) != devices.end()) distinct = false;
+            devices.push_back(ctxs[i]->cfg.device);
+        }
+        static const bool force_peer = [] {
+            const char* e = std::getenv("FW2V_AVERAGE");
+            return e != nullptr && std::strcmp(e, "peer") == 0;
+        }();
+        if (rule == kMergeMean || !distinct || force_peer || !nccl_available(nullptr)) {
+            // Mean: fw2v_average's path; others: one fused peer-memory kernel per
+            // member slice, the base shared from member 0.
+            if (rule == kMergeMean) {
+                average_impl(ctxs, n, nullptr, nullptr);
+                return local_sum;
+            }
+            average_impl(ctxs, 1, nullptr, nullptr);  // quiesce + shape checks on member 0
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) {
+                    if (devices[i] == devices[j]) continue;
+                    FW2V_CK(cudaSetDevice(devices[i]));
+                    cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else FW2V_CK(e);
+                }
+            for (int i = 0; i < n; ++i) {
+                FW2V_CK(cudaSetDevice(devices[i]));
+                FW2V_CK(cudaDeviceSynchronize());
+            }
+            for (int m = 0; m < 2; ++m) {
+                PeerSet ps{};
+                ps.n = n;
+                for (int i = 0; i < n; ++i) ps.ptr[i] = m == 0 ? ctxs[i]->syn0 : ctxs[i]->syn1;
+                float* base = x0->merge_base + m * count;
+                const size_t per = (count + n - 1) / n;
+                for (int g = 0; g < n; ++g) {
+                    FW2V_CK(cudaSetDevice(devices[g]));
+                    const size_t b = std::min(count, per * g), e = std::min(count, b + per);
+                    FW2V_CK(launch_merge_slice(ps, base, rule, b, e, nullptr));
+                }
+            }
+            for (int g = 0; g < n; ++g) {
+                FW2V_CK(cudaSetDevice(devices[g]));
+                FW2V_CK(cudaDeviceSynchronize());
+            }
+            return local_sum;
+        }
+    } else if (n != 1) {
+        fail(FW2V_ERR_UNSUPPORTED, "a multi-process job holds one context per process");
+    }
+    // Split merge: prep -> SUM all-reduce (NCCL clique or the exchange) -> finish.
+    std::string err;
+    if (!cross && (x0->clique == nullptr || x0->clique_members != std::vector<fw2v_ctx*>(ctxs, ctxs + n))) {
+        std::vector<int> devices;
+        for (int i = 0; i < n; ++i) devices.push_back(ctxs[i]->cfg.device);
+        auto c = nccl_clique_local(devices, &err);
+        if (!c) fail(FW2V_ERR_CUDA, err);
+        for (int i = 0; i < n; ++i) {
+            ctxs[i]->clique = c;
+            ctxs[i]->clique_members.assign(ctxs, ctxs + n);
+        }
+    }
+    std::vector<std::vector<float*>> bufs(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        fw2v_ctx* x = ctxs[i];
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        FW2V_CK(cudaDeviceSynchronize());
+        float* cnt = rule == kMergeTouched ? x->merge_cnt : nullptr;
+        FW2V_CK(launch_merge_prep(x->syn0, x->merge_base, cnt, rule, count, nullptr));
+        FW2V_CK(launch_merge_prep(x->syn1, x->merge_base + count, cnt ? cnt + count : nullptr, rule, count, nullptr));
+        FW2V_CK(cudaDeviceSynchronize());
+        bufs[static_cast<size_t>(i)] = {x->syn0, x->syn1};
+        if (cnt) {
+            bufs[static_cast<size_t>(i)].push_back(cnt);
+            bufs[static_cast<size_t>(i)].push_back(cnt + count);
+        }
+    }
+    uint64_t global = local_sum;
+    if (cross && exchange != nullptr) {
+        const std::vector<float*>& b = bufs[0];
+        std::vector<uint64_t> counts(b.size(), count);
+        const int rc = exchange(user, b.data(), counts.data(), static_cast<int32_t>(b.size()), local_sum, &global);
+        if (rc != FW2V_OK) fail(rc, "exchange callback failed");
+        FW2V_CK(cudaSetDevice(x0->cfg.device));
+        FW2V_CK(cudaDeviceSynchronize());
+    } else {
+        if (x0->clique == nullptr) fail(FW2V_ERR_BAD_ARGUMENT, "no communicator for a multi-process merge");
+        std::vector<unsigned long long*> words;
+        if (cross) {
+            FW2V_CK(cudaSetDevice(x0->cfg.device));
+            if (x0->d_words == nullptr) FW2V_CK(cudaMalloc(&x0->d_words, sizeof(unsigned long long)));
+            const unsigned long long w = local_sum;
+            FW2V_CK(cudaMemcpy(x0->d_words, &w, sizeof(w), cudaMemcpyHostToDevice));
+            words.push_back(x0->d_words);
+        }
+        if (!nccl_allreduce(*x0->clique, bufs, count, words, true, &err)) fail(FW2V_ERR_CUDA, err);
+        if (cross) {
+            unsigned long long w = 0;
+            FW2V_CK(cudaSetDevice(x0->cfg.device));
+            FW2V_CK(cudaMemcpy(&w, x0->d_words, sizeof(w), cudaMemcpyDeviceToHost));
+            global = w;
+        }
+    }
+    const float inv = 1.0f / static_cast<float>(n_total);
+    for (int i = 0; i < n; ++i) {
+        fw2v_ctx* x = ctxs[i];
+        FW2V_CK(cudaSetDevice(x->cfg.device));
+        float* cnt = rule == kMergeTouched ? x->merge_cnt : nullptr;
+        FW2V_CK(launch_merge_finish(x->syn0, x->merge_base, cnt, rule, inv, count, nullptr));
+        FW2V_CK(launch_merge_finish(x->syn1, x->merge_base ? x->merge_base + count : nullptr, cnt ? cnt + count : nullptr,
+                                    rule, inv, count, nullptr));
+        FW2V_CK(cudaDeviceSynchronize());
+    }
+    return global;
 }
 
 // The job's chunk partition for data-parallel runs: the reference's `workers`
@@ -1605,6 +1757,8 @@ int fw2v_train_corpus_multi(fw2v_ctx* const* ctxs, int32_t n, int32_t shard0, in
         uint64_t global_words = 0;
         for (int i = 0; i < n; ++i) global_words = std::max(global_words, ctxs[i]->words_trained);
         sh.scale = static_cast<uint64_t>(n_shards / n);
+        const int rule = cfg.replica_merge;
+        for (int i = 0; i < n; ++i) merge_begin(ctxs[i], rule);
         fw2v_report rep{};
         rep.vocab_size = static_cast<uint64_t>(x0->vocab);
         uint64_t bw = 0, bn = 0;
@@ -1645,16 +1799,9 @@ int fw2v_train_corpus_multi(fw2v_ctx* const* ctxs, int32_t n, int32_t shard0, in
                     epoch_words += o.traffic.words;
                 }
                 rep.kernel_seconds += ks;
-                // Exchange: replicas <- their mean over every shard; the global word
-                // count is exact again (lr_at's position, trainer.cpp:479-487).
-                uint64_t g = 0;
-                average_impl(ctxs, n, lw.data(), &g);
-                if (exchange != nullptr) {
-                    uint64_t gg = g;
-                    const int rc = exchange(exchange_user, g, &gg);
-                    if (rc != FW2V_OK) fail(rc, "exchange callback failed");
-                    g = gg;
-                }
+                // Merge: replicas <- one model from every shard's round (replica_merge); the
+                // global word count is exact again (lr_at's position, trainer.cpp:479-487).
+                const uint64_t g = merge_impl(ctxs, n, n_shards, rule, lw.data(), exchange, exchange_user);
                 global_words += g;
             }
             for (int i = 0; i < n; ++i) ctxs[i]->words_trained = global_words;

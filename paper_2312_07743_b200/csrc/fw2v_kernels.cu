@@ -664,4 +664,78 @@ cudaError_t launch_average_slice(const PeerSet& ps, size_t begin, size_t end, cu
     return cudaGetLastError();
 }
 
+// Replica merge of data-parallel rounds (fw2v_config.replica_merge), element
+// by element, with b = the replicas' common value at the round start and
+// d_r = v_r - b each replica's round delta:
+//   mean     v = mean_r v_r                       (model averaging)
+//   touched  v = b + sum_r d_r / #{r : d_r != 0}  (mean over the replicas that
+//            changed the element: a row only one shard trained keeps its full
+//            update; rows every shard trained get the mean)
+//   sum      v = b + sum_r d_r                    (every update applied, Hogwild-like)
+__device__ __forceinline__ float merge_value(int rule, float b, float sum_d, float cnt, float inv_n, float sum_v) {
+    if (rule == kMergeMean) return sum_v * inv_n;
+    if (rule == kMergeSum) return b + sum_d;
+    return b + (cnt > 1.0f ? sum_d / cnt : sum_d);
+}
+
+// Fused peer-memory merge, member g's slice [begin, end) of every replica (see
+// k_average_slice).
+__global__ void k_merge_slice(PeerSet ps, float* base, int rule, size_t begin, size_t end) {
+    const float inv = 1.0f / static_cast<float>(ps.n);
+    const size_t nth = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t x = begin + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; x < end; x += nth) {
+        const float b = base != nullptr ? base[x] : 0.0f;
+        float sd = 0.0f, sv = 0.0f, c = 0.0f;
+        for (int r = 0; r < ps.n; ++r) {
+            const float v = ps.ptr[r][x];
+            const float d = v - b;
+            sv += v;
+            sd += d;
+            c += d != 0.0f ? 1.0f : 0.0f;
+        }
+        const float m = merge_value(rule, b, sd, c, inv, sv);
+        for (int r = 0; r < ps.n; ++r) ps.ptr[r][x] = m;
+        if (base != nullptr) base[x] = m;
+    }
+}
+cudaError_t launch_merge_slice(const PeerSet& ps, float* base, int rule, size_t begin, size_t end, cudaStream_t st) {
+    if (end <= begin || ps.n < 1) return cudaSuccess;
+    k_merge_slice<<<148 * 4, 256, 0, st>>>(ps, base, rule, begin, end);
+    return cudaGetLastError();
+}
+
+// Split merge around a SUM all-reduce (NCCL or the caller's exchange):
+// prep turns a replica into what is summed (v itself for mean; d = v - b and,
+// for touched, the indicator d != 0 into cnt), finish turns the sums into the
+// merged value and makes it the next round's base.
+__global__ void k_merge_prep(float* v, const float* base, float* cnt, int rule, size_t n) {
+    const size_t nth = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t x = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; x < n; x += nth) {
+        const float d = v[x] - base[x];
+        v[x] = d;
+        if (cnt != nullptr) cnt[x] = d != 0.0f ? 1.0f : 0.0f;
+    }
+}
+__global__ void k_merge_finish(float* v, float* base, const float* cnt, int rule, float inv_n, size_t n) {
+    const size_t nth = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t x = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; x < n; x += nth) {
+        const float s = v[x];
+        const float b = base != nullptr ? base[x] : 0.0f;
+        const float m = merge_value(rule, b, s, cnt != nullptr ? cnt[x] : 0.0f, inv_n, s);
+        v[x] = m;
+        if (base != nullptr) base[x] = m;
+    }
+}
+cudaError_t launch_merge_prep(float* v, const float* base, float* cnt, int rule, size_t n, cudaStream_t st) {
+    if (rule == kMergeMean || n == 0) return cudaSuccess;
+    k_merge_prep<<<148 * 4, 256, 0, st>>>(v, base, cnt, rule, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_merge_finish(float* v, float* base, const float* cnt, int rule, float inv_n, size_t n,
+                                cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_merge_finish<<<148 * 4, 256, 0, st>>>(v, rule == kMergeMean ? nullptr : base, cnt, rule, inv_n, n);
+    return cudaGetLastError();
+}
+
 } // namespace fw2v

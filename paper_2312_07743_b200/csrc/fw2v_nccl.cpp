@@ -149,18 +149,18 @@ std::shared_ptr<NcclClique> nccl_clique_rank(int device, const uint8_t id_bytes[
     return c;
 }
 
-// In place: every member's buffers[i] (count floats each, per matrix) <- the
-// mean over all members of all processes; u64[i] (may be null) <- the sum.
-// Synchronous: returns after every member's stream finished.
-bool nccl_average(NcclClique& c, const std::vector<std::vector<float*>>& buffers, size_t count,
-                  const std::vector<unsigned long long*>& u64, std::string* err) {
+// In place: every member's buffers[i] (count floats each) <- the mean (sum =
+// false) or the sum over all members of all processes; u64[i] (may be null) <-
+// the sum. Synchronous: returns after every member's stream finished.
+bool nccl_allreduce(NcclClique& c, const std::vector<std::vector<float*>>& buffers, size_t count,
+                    const std::vector<unsigned long long*>& u64, bool sum, std::string* err) {
     const NcclApi& a = api();
     if (!check(a.GroupStart(), "ncclGroupStart", err)) return false;
     bool ok = true;
     for (size_t i = 0; i < c.comms.size() && ok; ++i) {
         cudaSetDevice(c.devices[i]);
         for (float* b : buffers[i])
-            ok = ok && check(a.AllReduce(b, b, count, ncclFloat32, ncclAvg, c.comms[i], c.streams[i]), "ncclAllReduce", err);
+            ok = ok && check(a.AllReduce(b, b, count, ncclFloat32, sum ? ncclSum : ncclAvg, c.comms[i], c.streams[i]), "ncclAllReduce", err);
         if (ok && i < u64.size() && u64[i] != nullptr)
             ok = check(a.AllReduce(u64[i], u64[i], 1, ncclUint64, ncclSum, c.comms[i], c.streams[i]), "ncclAllReduce", err);
     }

@@ -12,9 +12,9 @@ in-process over ``ncclCommInitAll`` or across processes after
 
 This module holds the Python side of a multi-process job: sharding arithmetic
 and ``TorchExchange``, the exchange callback for process groups NCCL cannot
-serve (gloo on CPU, or several ranks sharing one GPU in tests): it averages
-model tensors attached to the trainer (``Trainer.attach_model``) with
-``torch.distributed`` and sums the word counts.
+serve (gloo on CPU, or several ranks sharing one GPU in tests): it SUMs the
+buffers the native trainer hands over with ``torch.distributed`` and sums the
+word counts.
 """
 from __future__ import annotations
 
@@ -81,22 +81,47 @@ def global_words(local_words: int, group=None) -> int:
     return int(t.item())
 
 
-class TorchExchange:
-    """Exchange callback for ``train_corpus_multi(..., exchange=...)``: averages
-    the attached replica tensor over the process group and returns the global
-    word count. Called by the native trainer after this process's kernels
-    finished (so the model is quiescent)."""
+class _DeviceView:
+    """Zero-copy torch view of a library-owned fp32 device buffer."""
 
-    def __init__(self, model, group=None):
-        self.averager = ReplicaAverager(model, group)
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+
+def device_tensor(ptr: int, count: int):
+    import torch
+
+    return torch.as_tensor(_DeviceView(ptr, count), device="cuda")
+
+
+class TorchExchange:
+    """Exchange callback for ``train_corpus_multi(..., exchange=...)``: SUMs the
+    buffers the native trainer hands over (its replicas turned into summands,
+    per ``replica_merge``) over the process group in place, and returns the
+    global word count. Called after this process's kernels finished. gloo
+    reduces through host copies."""
+
+    def __init__(self, group=None):
         self.group = group
         self.calls = 0
 
-    def __call__(self, local_words: int) -> int:
+    def __call__(self, buffers, local_words: int) -> int:
         import torch
+        import torch.distributed as dist
 
-        if self.averager.model.is_cuda:
-            torch.cuda.synchronize(self.averager.model.device)
-        self.averager.average()
+        cuda = torch.cuda.is_available()
+        if cuda:
+            torch.cuda.synchronize()
+        gloo = dist.get_backend(self.group) == "gloo"
+        for b in buffers:
+            t = b if isinstance(b, torch.Tensor) else device_tensor(*b)
+            if gloo and t.is_cuda:
+                host = t.cpu()
+                dist.all_reduce(host, op=dist.ReduceOp.SUM, group=self.group)
+                t.copy_(host)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        if cuda:
+            torch.cuda.synchronize()
         self.calls += 1
         return global_words(local_words, self.group)

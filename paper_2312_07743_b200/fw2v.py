@@ -28,6 +28,7 @@ DROPIN_PATH = os.path.join(LIB_DIR, "libringvec_fw2v.so")
 
 REUSE_MODES = {"lifetime": 0, "window": 1, "none": 2, "window_snapshot": 3}
 SAMPLERS = {"reference": 0, "alias": 1}
+MERGES = {"mean": 0, "touched": 1, "sum": 2}
 
 OK = 0
 ERR_NO_DEVICE = 66
@@ -67,7 +68,7 @@ class CConfig(C.Structure):
         ("device", C.c_int32), ("deterministic", C.c_int32), ("sampler", C.c_int32),
         ("fast_sigmoid", C.c_int32), ("k1_lanes", C.c_int32), ("streams", C.c_int32),
         ("l1_refresh_log2", C.c_int32), ("delta_writeback", C.c_int32), ("max_inflight", C.c_int32),
-        ("hot_rows", C.c_int32), ("hot_replicas", C.c_int32),
+        ("hot_rows", C.c_int32), ("hot_replicas", C.c_int32), ("replica_merge", C.c_int32),
     ]
 
 
@@ -95,7 +96,8 @@ class CReport(C.Structure):
 
 
 OBSERVER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_uint64)
-EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64))
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_int32, C.c_uint64,
+                          C.POINTER(C.c_uint64))
 EPOCH_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(CEpoch))
 
 
@@ -131,6 +133,7 @@ class TrainConfig:
     max_inflight: int = 0
     hot_rows: int = 64
     hot_replicas: int = 16
+    replica_merge: str = "touched"  # data-parallel rounds: mean | touched | sum (include/fw2v.h)
 
     @property
     def context_width(self) -> int:
@@ -144,6 +147,8 @@ class TrainConfig:
                 v = REUSE_MODES[v]
             elif f.name == "sampler":
                 v = SAMPLERS[v]
+            elif f.name == "replica_merge":
+                v = MERGES[v]
             elif isinstance(v, bool):
                 v = int(v)
             setattr(c, f.name, v)
@@ -487,7 +492,8 @@ def nccl_unique_id() -> bytes:
 def train_corpus_multi(trainers, corpus: Corpus, average_words: int = 0, shard0: int = 0, n_shards: int = 0,
                        exchange=None, on_epoch=None) -> Report:
     """Data-parallel training (fw2v_train_corpus_multi): trainer i trains shard shard0+i of n_shards
-    (default: len(trainers)); exchange(local_words) -> global_words averages across processes."""
+    (default: len(trainers)). exchange(buffers, local_words) -> global_words connects processes:
+    `buffers` are (device pointer, float count) pairs it must SUM over the processes in place."""
     offsets = np.ascontiguousarray(corpus.offsets, np.uint64)
     ids = np.ascontiguousarray(corpus.ids, np.int32)
     epochs = []
@@ -498,9 +504,9 @@ def train_corpus_multi(trainers, corpus: Corpus, average_words: int = 0, shard0:
         if on_epoch:
             on_epoch(epochs[-1])
 
-    def _ex(_u, local, out):
+    def _ex(_u, bufs, counts, n_bufs, local, out):
         try:
-            out[0] = int(exchange(int(local)))
+            out[0] = int(exchange([(bufs[i], counts[i]) for i in range(n_bufs)], int(local)))
             return 0
         except Exception:  # noqa: BLE001 - reported through the status code
             import traceback

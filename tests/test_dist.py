@@ -57,11 +57,11 @@ def _worker(rank, world, port, q):
         avg = ReplicaAverager(model)
         avg.average()
         words = global_words(1000 * (rank + 1))
-        # the exchange callback: replicas differ per element, words per rank
+        # the exchange callback: summands differ per element, words per rank
         rng = np.random.default_rng(rank)
         m2 = torch.from_numpy(rng.standard_normal((2, 7, 12)).astype(np.float32))
-        ex = TorchExchange(m2)
-        g = ex(123 + rank)
+        ex = TorchExchange()
+        g = ex([m2[0], m2[1]], 123 + rank)
         q.put((rank, model.mean().item(), float(model.std()), words, avg.rounds, m2.numpy().copy(), g, ex.calls))
     finally:
         dist.destroy_process_group()
@@ -78,7 +78,7 @@ def test_replica_average_gloo_world2():
     for p in procs:
         p.join(120)
         assert p.exitcode == 0
-    want = sum(np.random.default_rng(r).standard_normal((2, 7, 12)).astype(np.float32) for r in range(world)) / world
+    want = sum(np.random.default_rng(r).standard_normal((2, 7, 12)).astype(np.float32) for r in range(world))
     for rank, mean, std, words, rounds, m2, g, calls in res:
         assert mean == pytest.approx(0.5) and std == 0.0
         assert words == 3000 and rounds == 1

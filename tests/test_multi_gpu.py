@@ -78,7 +78,8 @@ def planted_ref(ref):
 
 @pytest.mark.parametrize("mode", ["lifetime", "window_snapshot"])
 @pytest.mark.parametrize("sampler", ["reference", "alias"])
-def test_train_multi_two_replicas(planted_ref, mode, sampler):
+@pytest.mark.parametrize("merge", ["touched", "sum", "mean"])
+def test_train_multi_two_replicas(planted_ref, mode, sampler, merge):
     """Two replicas, each a contiguous shard, averaged twice per epoch: the
     union of their batches is the reference's for workers=16 (exact global word
     and sentence counts), and loss / recall@10 match the reference within the
@@ -87,7 +88,8 @@ def test_train_multi_two_replicas(planted_ref, mode, sampler):
     ref_loss, ref_recall = _eval(rin, rout, offsets, ids, counts, word_topic)
     corpus = fw.Corpus(counts, offsets, ids)
     est = rrep.words_trained / CFG["epochs"] / 2  # words per shard and epoch
-    cfg = fw.TrainConfig(workers=16, deterministic=0, reuse_mode=mode, dim=64, sampler=sampler, **CFG)
+    cfg = fw.TrainConfig(workers=16, deterministic=0, reuse_mode=mode, dim=64, sampler=sampler, replica_merge=merge,
+                         **CFG)
     ts = [fw.Trainer(cfg, counts) for _ in range(2)]
     try:
         rep = fw.train_corpus_multi(ts, corpus, average_words=int(est / 2))
@@ -102,7 +104,7 @@ def test_train_multi_two_replicas(planted_ref, mode, sampler):
     np.testing.assert_array_equal(m[0][0], m[1][0])  # replicas equal after the final average
     np.testing.assert_array_equal(m[0][1], m[1][1])
     loss, recall = _eval(m[0][0], m[0][1], offsets, ids, counts, word_topic)
-    print(f"dp2 {mode} {sampler}: loss {loss:.4f} vs ref {ref_loss:.4f}; recall@10 {recall:.4f} vs {ref_recall:.4f}")
+    print(f"dp2 {mode} {sampler} {merge}: loss {loss:.4f} vs ref {ref_loss:.4f}; recall@10 {recall:.4f} vs {ref_recall:.4f}")
     assert abs(loss - ref_loss) / ref_loss <= 0.02
     assert recall >= ref_recall - 0.01
 
@@ -131,7 +133,6 @@ def _rank_main(rank, world, port, q):
 
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    import torch
     import torch.distributed as dist
 
     import paper_2312_07743_b200 as fw_
@@ -143,11 +144,7 @@ def _rank_main(rank, world, port, q):
         counts, offsets, ids, _ = pc()
         cfg = fw_.TrainConfig(workers=16, deterministic=0, reuse_mode="window_snapshot", dim=64, **cfg_)
         t = fw_.Trainer(cfg, counts)
-        model = torch.zeros((2, t.vocab, t.stride), dtype=torch.float32, device="cuda:0")
-        torch.cuda.synchronize()
-        t.attach_model(model[0].data_ptr(), model[1].data_ptr())
-        t.init_model(cfg.seed)
-        ex = TorchExchange(model)
+        ex = TorchExchange()
         rep = fw_.train_corpus_multi([t], fw_.Corpus(counts, offsets, ids), average_words=300_000, shard0=rank,
                                      n_shards=world, exchange=ex)
         gi, go = t.get_model()
