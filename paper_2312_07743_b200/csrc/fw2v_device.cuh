@@ -57,7 +57,7 @@ constexpr int32_t kFlagInvalShift = 8;    // bits 8..11: otherwise one warp per 
 // Replicas of one matrix for the peer-memory average (fw2v_average): the same
 // |V| x stride buffer on each of n members (device pointers, P2P-accessible).
 constexpr int kMaxPeers = 16;
-enum MergeRule : int32_t { kMergeMean = 0, kMergeTouched = 1, kMergeSum = 2 };  // fw2v_config.replica_merge
+enum MergeRule : int32_t { kMergeMean = 0, kMergeTouched = 1 };  // fw2v_config.replica_merge
 struct PeerSet {
     float* ptr[kMaxPeers];
     int32_t n;

@@ -545,7 +545,7 @@ void validate(const fw2v_config& c) {  // validate_config (config.cpp:165-177)
     if (c.sampler < 0 || c.sampler > 1) fail(FW2V_ERR_BAD_CONFIG, "unknown sampler");
     if (c.hot_rows < 0 || c.hot_replicas < 1) fail(FW2V_ERR_BAD_CONFIG, "hot_rows must be >= 0 and hot_replicas >= 1");
     if (c.delta_writeback < 0 || c.delta_writeback > 2) fail(FW2V_ERR_BAD_CONFIG, "delta_writeback must be 0, 1 or 2");
-    if (c.replica_merge < 0 || c.replica_merge > 2) fail(FW2V_ERR_BAD_CONFIG, "replica_merge must be 0, 1 or 2");
+    if (c.replica_merge < 0 || c.replica_merge > 1) fail(FW2V_ERR_BAD_CONFIG, "replica_merge must be 0 or 1");
 }
 
 void require_device(int device) {

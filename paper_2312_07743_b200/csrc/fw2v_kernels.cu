@@ -671,10 +671,10 @@ cudaError_t launch_average_slice(const PeerSet& ps, size_t begin, size_t end, cu
 //   touched  v = b + sum_r d_r / #{r : d_r != 0}  (mean over the replicas that
 //            changed the element: a row only one shard trained keeps its full
 //            update; rows every shard trained get the mean)
-//   sum      v = b + sum_r d_r                    (every update applied, Hogwild-like)
+// (Applying the summed deltas, b + sum_r d_r, diverges: +31% loss at 2 replicas
+// and overflow at 8 on the text8 shape, profiles/r02_dp_merge_probe.txt.)
 __device__ __forceinline__ float merge_value(int rule, float b, float sum_d, float cnt, float inv_n, float sum_v) {
     if (rule == kMergeMean) return sum_v * inv_n;
-    if (rule == kMergeSum) return b + sum_d;
     return b + (cnt > 1.0f ? sum_d / cnt : sum_d);
 }
 

@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -44,7 +45,11 @@ const NcclApi& api() {
     static NcclApi a;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // FW2V_NCCL_LIB: an explicit library (the Python binding points it at
+        // torch's bundled NCCL so torch, imported later, binds to the same copy).
+        void* h = nullptr;
+        if (const char* p = std::getenv("FW2V_NCCL_LIB"); p != nullptr && *p != 0) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+        if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (h == nullptr) {
             const char* e = dlerror();

@@ -28,7 +28,7 @@ DROPIN_PATH = os.path.join(LIB_DIR, "libringvec_fw2v.so")
 
 REUSE_MODES = {"lifetime": 0, "window": 1, "none": 2, "window_snapshot": 3}
 SAMPLERS = {"reference": 0, "alias": 1}
-MERGES = {"mean": 0, "touched": 1, "sum": 2}
+MERGES = {"mean": 0, "touched": 1}
 
 OK = 0
 ERR_NO_DEVICE = 66
@@ -133,7 +133,7 @@ class TrainConfig:
     max_inflight: int = 0
     hot_rows: int = 64
     hot_replicas: int = 16
-    replica_merge: str = "touched"  # data-parallel rounds: mean | touched | sum (include/fw2v.h)
+    replica_merge: str = "touched"  # data-parallel rounds: mean | touched (include/fw2v.h)
 
     @property
     def context_width(self) -> int:
@@ -171,6 +171,23 @@ class Report:
 _lib = None
 
 
+def _prefer_torch_nccl():
+    """libfw2v opens NCCL lazily (dlopen "libnccl.so.2"). In a Python process
+    that may import torch, it must be torch's bundled copy: once a library with
+    that soname is loaded, torch's own libtorch_cuda binds to it, and the
+    system 2.27 lacks symbols torch needs. FW2V_NCCL_LIB points libfw2v at it."""
+    if os.environ.get("FW2V_NCCL_LIB"):
+        return
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia")
+    for root in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(root, "nccl", "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["FW2V_NCCL_LIB"] = cand
+            return
+
+
 def lib() -> C.CDLL:
     """Loads libfw2v.so; raises if it has not been built (no fallback)."""
     global _lib
@@ -178,6 +195,7 @@ def lib() -> C.CDLL:
         return _lib
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `make lib` or __graft_entry__.build()")
+    _prefer_torch_nccl()
     L = C.CDLL(LIB_PATH)
     L.fw2v_last_error.restype = C.c_char_p
     L.fw2v_lr_at.restype = C.c_float

@@ -75,9 +75,9 @@ def _unigram_negatives(counts, n, seed):
 
 # (name, knobs, bound on ||gpu - ref|| / ||ref - init|| per matrix)
 KNOBS = [
-    ("fast_sigmoid", dict(fast_sigmoid=True, l1_refresh_log2=0, delta_writeback=0), 5e-3),
-    ("fast+overwrite", dict(fast_sigmoid=True, l1_refresh_log2=0, delta_writeback=2), 5e-3),
-    ("bench: fast+overwrite+l1_refresh5", dict(fast_sigmoid=True, l1_refresh_log2=5, delta_writeback=2), 2e-2),
+    ("fast_sigmoid", dict(fast_sigmoid=True, l1_refresh_log2=0, delta_writeback=0), 1e-4),
+    ("fast+overwrite", dict(fast_sigmoid=True, l1_refresh_log2=0, delta_writeback=2), 1e-4),
+    ("bench: fast+overwrite+l1_refresh5", dict(fast_sigmoid=True, l1_refresh_log2=5, delta_writeback=2), 1e-4),
 ]
 
 
@@ -88,7 +88,9 @@ def test_k1s_bench_knobs_per_sentence(text8, oracle, mode, dim, knobs):
     """One sentence per launch (no Hogwild interaction): the bench kernel's
     deviations from the reference order are the fast sigmoid (|err| < 1e-3) and,
     with l1_refresh_log2 = 5, a sentence re-reading a sample row it rewrote
-    within the last 32 windows from its SM's L1 (stale by those updates)."""
+    within the last 32 windows from its SM's L1 — except that K1s re-reads a row
+    the previous window rewrote, so inside one sentence the staging is exact.
+    Measured (r02): relative update error <= 2e-6 for every knob set.)"""
     name, kn, bound = knobs
     n, L, n_neg = 6, 160, 5
     offsets, ids = _zipf_sentences(text8, n, L, seed=dim)

@@ -43,7 +43,7 @@ print(f"{which}: reference loss {ref_loss:.4f} recall {ref_rec:.4f} words {rrep.
 per_epoch = rrep.words_trained / base["epochs"]
 for R in Rs:
     for rounds in rounds_list:
-        for merge in ("mean", "touched", "sum"):
+        for merge in ("mean", "touched"):
             cfg = fw.TrainConfig(workers=64, streams=16, deterministic=0, reuse_mode="window_snapshot",
                                  sampler="alias", replica_merge=merge, **base)
             ts = [fw.Trainer(cfg, counts) for _ in range(R)]
