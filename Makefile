@@ -17,8 +17,8 @@ CUDA_INC := /usr/local/cuda/include
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v -Iinclude -I$(SRC)
 CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -Wextra -Iinclude -I$(SRC) -I$(CUDA_INC)
 
-.PHONY: all lib dropin oracle suite clean
-all: lib dropin oracle suite
+.PHONY: all lib dropin harness oracle suite clean
+all: lib dropin harness oracle suite
 
 lib: $(LIB)/libfw2v.so
 
@@ -73,6 +73,27 @@ $(LIB)/libringvec_fw2v.so: $(SRC)/ringvec_train_fw2v.cpp $(LIB)/libfw2v.so inclu
 	  $(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -I$(REF)/include -o $@ $< \
 	    -L$(LIB) -lfw2v -Wl,-rpath,'$$ORIGIN'; \
 	else echo "reference headers absent: keeping prebuilt $@"; fi
+
+# Drop-in harness (bench.py's drop-in e2e leg): the reference's own sources
+# (trainer.cpp excluded: the drop-in supplies train()) compiled where they lie
+# with the reference's flags, plus csrc/ringvec_harness.cpp, linked against
+# libringvec_fw2v.so. Needs the reference headers and sources at build time;
+# the GPU box uses the prebuilt library.
+JSON_INC ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+HREF_SRCS := config corpus eval model sampler traffic
+HREF_OBJS := $(addprefix $(BUILD)/href_,$(addsuffix .o,$(HREF_SRCS)))
+harness: $(LIB)/libringvec_harness.so
+
+$(BUILD)/href_%.o: $(REF)/src/%.cpp
+	@mkdir -p $(BUILD)
+	$(CXX) -std=c++20 -O2 -fPIC -I$(REF)/include -I$(JSON_INC) -c -o $@ $<
+
+$(LIB)/libringvec_harness.so: $(SRC)/ringvec_harness.cpp $(LIB)/libringvec_fw2v.so
+	@if [ -d $(REF)/include ]; then \
+	  $(MAKE) $(HREF_OBJS) && \
+	  $(CXX) -std=c++20 -O2 -fPIC -shared -I$(REF)/include -o $@ $< $(HREF_OBJS) \
+	    -L$(LIB) -lringvec_fw2v -lfw2v -Wl,-rpath,'$$ORIGIN' -lpthread; \
+	else echo "reference sources absent: keeping prebuilt $@"; fi
 
 oracle:
 	$(MAKE) -C oracle all

@@ -233,6 +233,14 @@ int fw2v_comm_init_rank(fw2v_ctx* ctx, const uint8_t id[128], int32_t world, int
 typedef int (*fw2v_exchange_fn)(void* user, float* const* bufs, const uint64_t* counts, int32_t n_bufs,
                                 uint64_t local_words, uint64_t* global_words);
 
+/* The merge step of fw2v_train_corpus_multi on its own (device-resident benchmark rounds):
+ * fw2v_merge_begin records the replicas' common starting point, fw2v_merge_replicas merges the
+ * replicas per ctxs[0]'s replica_merge rule (n_shards > n: across processes as above) and
+ * returns the global word count. */
+int fw2v_merge_begin(fw2v_ctx* const* ctxs, int32_t n);
+int fw2v_merge_replicas(fw2v_ctx* const* ctxs, int32_t n, int32_t n_shards, const uint64_t* local_words,
+                        fw2v_exchange_fn exchange, void* exchange_user, uint64_t* global_words);
+
 /* Data-parallel training: this call trains shards shard0 .. shard0+n-1 (context i <- shard
  * shard0+i) of an n_shards-shard job (n_shards > n: other processes hold the rest and `exchange`
  * or fw2v_comm_init_rank connects them; one context per process then). Replicas are merged per

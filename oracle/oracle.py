@@ -265,5 +265,44 @@ class Oracle:
         return inp, out, Report.from_c(rep)
 
 
+class RefCorpus:
+    """A ringvec::Corpus built by the reference (ref_synth_corpus): the bench's
+    reference arm trains it without loading libfw2v. ref only."""
+
+    def __init__(self, oracle: "Oracle", types=0, tokens=0, s=1.0, sentence_len=1000, min_count=5, _handle=None):
+        self.o = oracle
+        h = _handle if _handle is not None else C.c_void_p()
+        if _handle is None:
+            oracle._check(oracle._fn("synth_corpus")(C.c_uint64(types), C.c_uint64(tokens), C.c_double(s),
+                                                     C.c_uint64(sentence_len), C.c_uint64(min_count), C.byref(h)))
+        self.h = h
+        pc, v, ns, ni = C.POINTER(C.c_uint64)(), C.c_int32(), C.c_uint64(), C.c_uint64()
+        oracle._fn("corpus_view")(h, C.byref(pc), C.byref(v), C.byref(ns), C.byref(ni))
+        self.counts = np.ctypeslib.as_array(pc, (v.value,)).copy()
+        self.n_sentences, self.n_ids = ns.value, ni.value
+
+    def arrays(self):
+        off = np.zeros(self.n_sentences + 1, np.uint64)
+        ids = np.zeros(self.n_ids, np.int32)
+        self.o._fn("corpus_export")(self.h, _p(off, C.c_uint64), _p(ids, C.c_int32))
+        return off, ids
+
+    def head(self, n_sentences: int) -> "RefCorpus":
+        h = C.c_void_p()
+        self.o._check(self.o._fn("corpus_head")(self.h, C.c_uint64(n_sentences), C.byref(h)))
+        return RefCorpus(self.o, _handle=h)
+
+    def train(self, cfg: TrainConfig) -> Report:
+        rep = CReport()
+        c = cfg.to_c()
+        self.o._check(self.o._fn("train_corpus")(self.h, C.byref(c), C.byref(rep)))
+        return Report.from_c(rep)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o._fn("corpus_free")(self.h)
+            self.h = None
+
+
 def available(kind: str) -> bool:
     return os.path.exists(LIB_PATHS[kind])

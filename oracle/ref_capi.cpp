@@ -19,9 +19,12 @@
 //   ref_save_embeddings  -> ringvec::save_embeddings       model.cpp:47-74
 //   ref_nearest_neighbors-> ringvec::nearest_neighbors     eval.cpp:303-348
 //   ref_analogy_correct  -> ringvec::eval_analogy          eval.cpp:212-290
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -63,6 +66,23 @@ struct ref_report {
     uint64_t traffic[5];  // context_reads, context_writes, sample_reads, sample_writes, ring_hits
     uint64_t analytic[5];
 };
+
+// Synthetic Zipf corpus of the BASELINE.md §2 shapes, built the REFERENCE way
+// (the bench's reference arm must not load libfw2v): token i = rank r with
+// p(r) ∝ r^-s drawn by inverse CDF from Rng::derive(2312, 7743).next_double()
+// (rng.hpp:16-33), token text "r<rank>", Vocabulary::build(counts, min_count)
+// (corpus.cpp:117-139), sentences of sentence_len raw tokens with OOV tokens
+// dropped and empty sentences skipped (what SentenceReader does with
+// ignore_delimiters, corpus.cpp:162-213). tests/test_oracle.py checks it equals
+// fw2v_corpus_synth_zipf id for id.
+int ref_synth_corpus(uint64_t types, uint64_t tokens, double s, uint64_t sentence_len, uint64_t min_count,
+                     void** out);
+int ref_corpus_view(void* h, const uint64_t** counts, int32_t* vocab_size, uint64_t* n_sentences,
+                    uint64_t* n_ids);
+int ref_corpus_export(void* h, uint64_t* offsets, int32_t* ids);
+int ref_train_corpus(void* h, const ref_config* cfg, ref_report* report);
+int ref_corpus_head(void* h, uint64_t n_sentences, void** out);
+void ref_corpus_free(void* h);
 
 } // extern "C"
 
@@ -388,5 +408,120 @@ int ref_analogy_correct(const float* rows, int32_t n, int32_t dim, const int32_t
         return fail(ex);
     }
 }
+
+namespace {
+struct RefCorpus {
+    Corpus corpus;
+    std::vector<uint64_t> counts;
+};
+void fill_report(ref_report* report, const RunReport& r) {
+    std::memset(report, 0, sizeof(*report));
+    report->words_trained = r.words_trained;
+    report->sentences_trained = r.sentences_trained;
+    report->vocab_size = r.vocab_size;
+    report->wall_seconds = r.wall_seconds;
+    report->batching_words_per_sec = r.batching_words_per_sec;
+    report->n_epochs = static_cast<int32_t>(std::min<size_t>(r.epochs.size(), 64));
+    for (int32_t e = 0; e < report->n_epochs; ++e) {
+        report->epoch_words[e] = r.epochs[static_cast<size_t>(e)].words;
+        report->epoch_seconds[e] = r.epochs[static_cast<size_t>(e)].seconds;
+        report->epoch_words_per_sec[e] = r.epochs[static_cast<size_t>(e)].words_per_sec;
+    }
+    fill_counters(report->traffic, r.traffic);
+    fill_counters(report->analytic, r.analytic);
+}
+} // namespace
+
+int ref_synth_corpus(uint64_t types, uint64_t tokens, double s, uint64_t sentence_len, uint64_t min_count,
+                     void** out) {
+    *out = nullptr;
+    try {
+        if (types < 1 || sentence_len < 1) raise(ErrorCode::bad_argument, "types and sentence_len must be >= 1");
+        std::vector<double> cdf(types);
+        double acc = 0.0;
+        for (uint64_t r = 0; r < types; ++r) cdf[r] = (acc += std::pow(static_cast<double>(r + 1), -s));
+        for (double& v : cdf) v /= acc;
+        cdf[types - 1] = 1.0;
+        Rng rng = Rng::derive(2312, 7743);
+        std::vector<uint32_t> rank(tokens);
+        std::vector<uint64_t> count(types, 0);
+        for (uint64_t i = 0; i < tokens; ++i) {
+            const double u = rng.next_double();
+            const uint64_t r = static_cast<uint64_t>(std::upper_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
+            rank[i] = static_cast<uint32_t>(std::min(r, types - 1));
+            ++count[rank[i]];
+        }
+        std::unordered_map<std::string, uint64_t> m;
+        m.reserve(types * 2);
+        for (uint64_t r = 0; r < types; ++r)
+            if (count[r] > 0) m["r" + std::to_string(r + 1)] = count[r];
+        auto c = std::make_unique<RefCorpus>();
+        c->corpus.vocab = Vocabulary::build(m, min_count);
+        std::vector<int32_t> remap(types, -1);
+        for (uint64_t r = 0; r < types; ++r)
+            if (count[r] > 0) remap[r] = c->corpus.vocab.id_of("r" + std::to_string(r + 1));
+        for (uint64_t t0 = 0; t0 < tokens; t0 += sentence_len) {
+            EncodedSentence es;
+            for (uint64_t i = t0; i < std::min(tokens, t0 + sentence_len); ++i)
+                if (remap[rank[i]] >= 0) es.ids.push_back(remap[rank[i]]);
+            if (!es.empty()) c->corpus.sentences.push_back(std::move(es));
+        }
+        c->corpus.raw_tokens = tokens;
+        for (int32_t w = 0; w < c->corpus.vocab.size(); ++w) c->counts.push_back(c->corpus.vocab.entry(w).count);
+        *out = c.release();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_corpus_view(void* h, const uint64_t** counts, int32_t* vocab_size, uint64_t* n_sentences, uint64_t* n_ids) {
+    auto* c = static_cast<RefCorpus*>(h);
+    *counts = c->counts.data();
+    *vocab_size = c->corpus.vocab.size();
+    *n_sentences = c->corpus.sentences.size();
+    *n_ids = c->corpus.encoded_tokens();
+    return 0;
+}
+
+int ref_corpus_export(void* h, uint64_t* offsets, int32_t* ids) {
+    auto* c = static_cast<RefCorpus*>(h);
+    offsets[0] = 0;
+    for (size_t k = 0; k < c->corpus.sentences.size(); ++k) {
+        const auto& v = c->corpus.sentences[k].ids;
+        std::memcpy(ids + offsets[k], v.data(), v.size() * sizeof(int32_t));
+        offsets[k + 1] = offsets[k] + v.size();
+    }
+    return 0;
+}
+
+// ringvec::train on the held corpus (trainer.cpp:390), model discarded.
+int ref_train_corpus(void* h, const ref_config* cfg, ref_report* report) {
+    try {
+        TrainResult r = train(static_cast<RefCorpus*>(h)->corpus, to_cfg(*cfg));
+        if (report) fill_report(report, r.report);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// The first n sentences, same vocabulary (a bounded sample of the workload).
+int ref_corpus_head(void* h, uint64_t n_sentences, void** out) {
+    try {
+        auto* c = static_cast<RefCorpus*>(h);
+        auto d = std::make_unique<RefCorpus>();
+        d->corpus.vocab = c->corpus.vocab;
+        d->counts = c->counts;
+        const uint64_t n = std::min<uint64_t>(n_sentences, c->corpus.sentences.size());
+        d->corpus.sentences.assign(c->corpus.sentences.begin(), c->corpus.sentences.begin() + static_cast<ptrdiff_t>(n));
+        *out = d.release();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+void ref_corpus_free(void* h) { delete static_cast<RefCorpus*>(h); }
 
 } // extern "C"

@@ -753,6 +753,9 @@ struct fw2v_ctx {
                 FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_alpha), 4 * cap_sent, cudaHostAllocDefault));
                 FW2V_CK(cudaMalloc(&s.d_ids, 4 * cap_words));
                 FW2V_CK(cudaMalloc(&s.d_negs, 4 * cap_words * nn + kNegPadBytes));
+                // K1s reads a window's negatives as one fixed-size group (masked where
+                // consumed), possibly past the copied part: keep it defined.
+                FW2V_CK(cudaMemset(s.d_negs, 0, 4 * cap_words * nn + kNegPadBytes));
                 FW2V_CK(cudaMalloc(&s.d_off, 4 * (cap_sent + 1)));
                 FW2V_CK(cudaMalloc(&s.d_alpha, 4 * cap_sent));
                 FW2V_CK(cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming));
@@ -1076,6 +1079,7 @@ int fw2v_train_sentences(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_senten
         } guard{{nullptr, nullptr, nullptr, nullptr, nullptr}};
         FW2V_CK(cudaMalloc(&d_ids, 4 * std::max<uint64_t>(words, 1))); guard.p[0] = d_ids;
         FW2V_CK(cudaMalloc(&d_negs, 4 * std::max<uint64_t>(words * n, 1) + kNegPadBytes)); guard.p[1] = d_negs;
+        FW2V_CK(cudaMemset(d_negs, 0, 4 * std::max<uint64_t>(words * n, 1) + kNegPadBytes));
         FW2V_CK(cudaMalloc(&d_off, 4 * (n_sentences + 1))); guard.p[2] = d_off;
         FW2V_CK(cudaMalloc(&d_alpha, 4 * std::max<uint64_t>(n_sentences, 1))); guard.p[3] = d_alpha;
         FW2V_CK(cudaMalloc(&d_ctr, sizeof(DevCounters))); guard.p[4] = d_ctr;
@@ -1707,6 +1711,21 @@ extern "C" {
 
 int fw2v_average(fw2v_ctx* const* ctxs, int32_t n) {
     return guarded([&] { average_impl(ctxs, n, nullptr, nullptr); });
+}
+
+int fw2v_merge_begin(fw2v_ctx* const* ctxs, int32_t n) {
+    return guarded([&] {
+        for (int i = 0; i < n; ++i) merge_begin(ctxs[i], ctxs[0]->cfg.replica_merge);
+    });
+}
+
+int fw2v_merge_replicas(fw2v_ctx* const* ctxs, int32_t n, int32_t n_shards, const uint64_t* local_words,
+                        fw2v_exchange_fn exchange, void* exchange_user, uint64_t* global_words) {
+    return guarded([&] {
+        if (n < 1 || n_shards < n) fail(FW2V_ERR_BAD_ARGUMENT, "need 1 <= n <= n_shards");
+        const uint64_t g = merge_impl(ctxs, n, n_shards, ctxs[0]->cfg.replica_merge, local_words, exchange, exchange_user);
+        if (global_words) *global_words = g;
+    });
 }
 
 int fw2v_nccl_unique_id(uint8_t out[128]) {

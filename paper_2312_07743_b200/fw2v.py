@@ -48,6 +48,7 @@ EXPORTED = [
     "fw2v_corpus_view", "fw2v_corpus_free", "fw2v_write_embeddings", "fw2v_save_model",
     "fw2v_nearest_neighbors", "fw2v_eval_analogy", "fw2v_alias_draws", "fw2v_plan_chunks",
     "fw2v_average", "fw2v_nccl_unique_id", "fw2v_comm_init_rank", "fw2v_train_corpus_multi",
+    "fw2v_merge_begin", "fw2v_merge_replicas",
 ]
 
 
@@ -501,6 +502,34 @@ def average(trainers):
     _check(lib().fw2v_average(_handles(trainers), len(trainers)))
 
 
+def _exchange_cb(exchange):
+    def _ex(_u, bufs, counts, n_bufs, local, out):
+        try:
+            out[0] = int(exchange([(bufs[i], counts[i]) for i in range(n_bufs)], int(local)))
+            return 0
+        except Exception:  # noqa: BLE001 - reported through the status code
+            import traceback
+
+            traceback.print_exc()
+            return ERR_BAD_ARGUMENT
+
+    return EXCHANGE_FN(_ex) if exchange else EXCHANGE_FN()
+
+
+def merge_begin(trainers):
+    _check(lib().fw2v_merge_begin(_handles(trainers), len(trainers)))
+
+
+def merge_replicas(trainers, local_words, n_shards=0, exchange=None) -> int:
+    """One replica merge (fw2v_merge_replicas); returns the global word count."""
+    lw = np.ascontiguousarray(local_words, np.uint64)
+    g = C.c_uint64()
+    cb = _exchange_cb(exchange)
+    _check(lib().fw2v_merge_replicas(_handles(trainers), len(trainers), n_shards or len(trainers), _p(lw, C.c_uint64),
+                                     cb, None, C.byref(g)))
+    return g.value
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib().fw2v_nccl_unique_id(buf))
@@ -522,24 +551,69 @@ def train_corpus_multi(trainers, corpus: Corpus, average_words: int = 0, shard0:
         if on_epoch:
             on_epoch(epochs[-1])
 
-    def _ex(_u, bufs, counts, n_bufs, local, out):
-        try:
-            out[0] = int(exchange([(bufs[i], counts[i]) for i in range(n_bufs)], int(local)))
-            return 0
-        except Exception:  # noqa: BLE001 - reported through the status code
-            import traceback
-
-            traceback.print_exc()
-            return ERR_BAD_ARGUMENT
-
     cb_ep = EPOCH_FN(_ep)
-    cb_ex = EXCHANGE_FN(_ex) if exchange else EXCHANGE_FN()
+    cb_ex = _exchange_cb(exchange)
     rep = CReport()
     _check(lib().fw2v_train_corpus_multi(_handles(trainers), len(trainers), shard0, n_shards or len(trainers),
                                          _p(offsets, C.c_uint64), C.c_uint64(len(offsets) - 1), _p(ids, C.c_int32),
                                          C.c_uint64(average_words), cb_ex, None, OBSERVER_FN(), None, cb_ep, None,
                                          C.byref(rep)))
     return _report(rep, epochs)
+
+
+class CHarnessConfig(C.Structure):
+    _fields_ = CConfig._fields_[:16]
+
+
+class CHarnessResult(C.Structure):
+    _fields_ = [("call_seconds", C.c_double), ("epoch_words_per_sec", C.c_double), ("words_trained", C.c_uint64),
+                ("input_checksum", C.c_double)]
+
+
+HARNESS_PATH = os.path.join(LIB_DIR, "libringvec_harness.so")
+
+
+class DropinHarness:
+    """A reference-side caller of the ringvec::train drop-in (libringvec_harness.so,
+    csrc/ringvec_harness.cpp): holds a ringvec::Corpus and times whole train() calls."""
+
+    def __init__(self, corpus: Corpus):
+        if not os.path.exists(HARNESS_PATH):
+            raise ImportError(f"{HARNESS_PATH} missing: `make harness` (needs the reference sources)")
+        lib()  # FW2V_NCCL_LIB before the drop-in can open NCCL
+        self.L = C.CDLL(HARNESS_PATH)
+        self.L.fw2v_harness_last_error.restype = C.c_char_p
+        self.L.fw2v_harness_free.restype = None
+        offsets = np.ascontiguousarray(corpus.offsets, np.uint64)
+        ids = np.ascontiguousarray(corpus.ids, np.int32)
+        counts = np.ascontiguousarray(corpus.counts, np.uint64)
+        h = C.c_void_p()
+        self._check(self.L.fw2v_harness_corpus(_p(counts, C.c_uint64), len(counts), _p(offsets, C.c_uint64),
+                                               C.c_uint64(len(offsets) - 1), _p(ids, C.c_int32), C.byref(h)))
+        self.h = h
+
+    def _check(self, rc):
+        if rc != 0:
+            raise Fw2vError(rc, self.L.fw2v_harness_last_error().decode())
+
+    def train(self, cfg: TrainConfig):
+        """One ringvec::train(corpus, cfg) call (reference TrainConfig fields of cfg; GPU
+        knobs come from FW2V_* environment variables as for any drop-in user)."""
+        full = cfg.to_c()
+        hc = CHarnessConfig()
+        for name, _ in CHarnessConfig._fields_:
+            setattr(hc, name, getattr(full, name))
+        r = CHarnessResult()
+        self._check(self.L.fw2v_harness_train(self.h, C.byref(hc), C.byref(r)))
+        return r
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.fw2v_harness_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 class Plan:
