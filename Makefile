@@ -29,7 +29,7 @@ $(BUILD)/fw2v_kernels.o: $(SRC)/fw2v_kernels.cu $(SRC)/fw2v_device.cuh
 # K1s: one translation unit per lane shape (compiled in parallel), plus the dispatch.
 K1S_SHAPES := l4v4 l8v4 l16v4 l16v8 l32v4 l32v6 l32v8 l32v10 l32v12 l32v16 l64v8
 K1S_OBJS   := $(addprefix $(BUILD)/k1s_,$(addsuffix .o,$(K1S_SHAPES)))
-K1S_DEPS   := $(SRC)/fw2v_snapshot.cuh $(SRC)/fw2v_device.cuh $(SRC)/fw2v_common.cuh
+K1S_DEPS   := $(SRC)/fw2v_snapshot.cuh $(SRC)/fw2v_stair.cuh $(SRC)/fw2v_device.cuh $(SRC)/fw2v_common.cuh
 
 $(BUILD)/k1s_%.o: $(SRC)/k1s_%.cu $(K1S_DEPS)
 	@mkdir -p $(BUILD)

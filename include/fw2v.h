@@ -37,7 +37,8 @@ enum fw2v_status {
     FW2V_ERR_ZERO_VECTOR = 12,
     FW2V_ERR_CUDA = 64,        /* CUDA runtime failure (message has the CUDA error string) */
     FW2V_ERR_UNSUPPORTED = 65, /* shape the B200 kernels do not cover (e.g. W_f > 5 on K1) */
-    FW2V_ERR_NO_DEVICE = 66    /* no CUDA device: there is no CPU fallback by design */
+    FW2V_ERR_NO_DEVICE = 66,   /* no CUDA device: there is no CPU fallback by design */
+    FW2V_ERR_DIVERGED = 67     /* Hogwild training stayed non-finite after the divergence guard's retries */
 };
 
 enum fw2v_reuse_mode { /* ringvec::ReuseMode (traffic.hpp:15) */
@@ -97,6 +98,10 @@ typedef struct fw2v_config {
                               one shard trained keeps its full update, others get the mean);
                               2 sum: b + sum d_r (every update applied, like Hogwild with the round as
                               staleness) */
+    int32_t divergence_guard; /* Hogwild fw2v_train_corpus: 1 = keep the model of the epoch start in HBM
+                                 and check the model is finite after the epoch; if not, restore it,
+                                 halve the in-flight budget and train the epoch again (up to 4 times,
+                                 then FW2V_ERR_DIVERGED). 0 = off (no snapshot, no check) */
 } fw2v_config;
 
 enum fw2v_replica_merge { FW2V_MERGE_MEAN = 0, FW2V_MERGE_TOUCHED = 1, FW2V_MERGE_SUM = 2 };
@@ -125,6 +130,7 @@ typedef struct fw2v_report {
     double kernel_seconds;  /* device span of the training passes (CUDA events on the launching streams,
                                pass start to last kernel completion), summed over passes */
     uint64_t h2d_bytes;     /* bytes copied host->device by the batch pipeline */
+    int32_t guard_retries;  /* epochs the divergence guard restored and trained again */
 } fw2v_report;
 
 /* Called once per target, in processing order, replayed per batch

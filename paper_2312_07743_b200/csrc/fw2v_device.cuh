@@ -51,6 +51,8 @@ constexpr int32_t kFlagL1Exact = 2;       // K1s sample rows are staged through 
 constexpr int32_t kFlagDeltaRing = 4;     // ring rows written back as red.add(final - loaded)
 constexpr int32_t kFlagNoRing = 32;       // K1s: ring rows stored straight back (Hogwild overwrite, no
                                           // shared-memory ring copy)
+constexpr int32_t kFlagNoStair = 64;      // K1s lifetime order: one window at a time (no window staircase;
+                                          // A/B experiments, FW2V_NO_STAIR=1)
 constexpr int32_t kFlagInvalShift = 8;    // bits 8..11: otherwise one warp per block drops the SM's L1 every
                                           // 2^k windows (bounded staleness for Zipf-hot rows; 0 = never)
 

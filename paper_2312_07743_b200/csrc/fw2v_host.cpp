@@ -47,6 +47,7 @@ cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf,
 cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st);
 // Hot-row replicas: average = false broadcasts syn1 rows 0..K-1 into them, true averages them back.
 cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st);
+cudaError_t launch_nonfinite(const float* p, size_t n, int* flag, cudaStream_t st);
 // K1s family: window-snapshot order, or (lifetime = true) the reference's lifetime order as a wavefront.
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
                        bool lifetime, DevCounters* ctr, cudaStream_t st, int* resident = nullptr);
@@ -624,6 +625,10 @@ struct fw2v_ctx {
     // for the touched rule, the changed-element indicators; [syn0 | syn1] each.
     float* merge_base = nullptr;
     float* merge_cnt = nullptr;
+    // Divergence guard (fw2v_config.divergence_guard): the model at the start
+    // of the current epoch, [syn0 | syn1], and a device flag word.
+    float* guard_snap = nullptr;
+    int* guard_flag = nullptr;
     size_t model_floats() const { return static_cast<size_t>(vocab) * static_cast<size_t>(stride); }
 
     int32_t k1_flags = 0;
@@ -782,6 +787,8 @@ struct fw2v_ctx {
         cudaFree(d_words);
         cudaFree(merge_base);
         cudaFree(merge_cnt);
+        cudaFree(guard_snap);
+        cudaFree(guard_flag);
         cudaFree(hot_alloc);
         if (own_model) {
             cudaFree(syn0);
@@ -891,6 +898,7 @@ void fw2v_config_default(fw2v_config* c) {
     c->hot_rows = 64;
     c->hot_replicas = 16;
     c->replica_merge = FW2V_MERGE_TOUCHED;
+    c->divergence_guard = 1;
 }
 
 int fw2v_validate_config(const fw2v_config* cfg) {
@@ -929,6 +937,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         x->k1_flags = kFlagRedSamples | (cfg->delta_writeback != 0 ? kFlagDeltaRing : 0) |
                       (cfg->delta_writeback == 2 ? kFlagNoRing : 0);
         x->k1_flags |= cfg->l1_refresh_log2 > 0 ? (std::min(cfg->l1_refresh_log2, 15) << kFlagInvalShift) : kFlagL1Exact;
+        if (const char* f = std::getenv("FW2V_NO_STAIR"); f != nullptr && *f != 0 && *f != '0') x->k1_flags |= kFlagNoStair;
         if (const char* f = std::getenv("FW2V_K1_FLAGS")) x->k1_flags = std::atoi(f);  // experiments
         x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
                             : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives, cfg->alpha0, 0, 1, cfg->dim) : 0;
@@ -1397,6 +1406,46 @@ void accumulate(fw2v_report& rep, const PassOut& o) {
     rep.h2d_bytes += o.h2d;
 }
 
+// ------------------------------------------------------ divergence guard
+constexpr int kGuardRetries = 4;
+
+void guard_save(fw2v_ctx* x) {
+    const size_t n = x->model_floats();
+    if (x->guard_snap == nullptr) {
+        FW2V_CK(cudaMalloc(&x->guard_snap, 2 * n * sizeof(float)));
+        FW2V_CK(cudaMalloc(&x->guard_flag, sizeof(int)));
+    }
+    FW2V_CK(cudaMemcpyAsync(x->guard_snap, x->syn0, n * sizeof(float), cudaMemcpyDeviceToDevice, nullptr));
+    FW2V_CK(cudaMemcpyAsync(x->guard_snap + n, x->syn1, n * sizeof(float), cudaMemcpyDeviceToDevice, nullptr));
+    FW2V_CK(cudaMemsetAsync(x->guard_flag, 0, sizeof(int), nullptr));
+    FW2V_CK(cudaStreamSynchronize(nullptr));
+}
+
+bool guard_finite(fw2v_ctx* x) {
+    const size_t n = x->model_floats();
+    FW2V_CK(launch_nonfinite(x->syn0, n, x->guard_flag, nullptr));
+    FW2V_CK(launch_nonfinite(x->syn1, n, x->guard_flag, nullptr));
+    int flag = 0;
+    FW2V_CK(cudaMemcpy(&flag, x->guard_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    return flag == 0;
+}
+
+void guard_restore(fw2v_ctx* x) {
+    const size_t n = x->model_floats();
+    FW2V_CK(cudaMemcpy(x->syn0, x->guard_snap, n * sizeof(float), cudaMemcpyDeviceToDevice));
+    FW2V_CK(cudaMemcpy(x->syn1, x->guard_snap + n, n * sizeof(float), cudaMemcpyDeviceToDevice));
+}
+
+void guard_halve_inflight(fw2v_ctx* x) {
+    int64_t cur = x->inflight_total;
+    if (cur <= 0) {  // uncapped: start from what the device holds at once
+        int resident = 0;
+        FW2V_CK(x->launch_one(BatchView{}, false, nullptr, nullptr, &resident));
+        cur = resident > 0 ? resident : 4096;
+    }
+    x->inflight_total = std::max<int64_t>(1, cur / 2);
+}
+
 } // namespace
 
 extern "C" {
@@ -1418,11 +1467,30 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
         rep.vocab_size = static_cast<uint64_t>(x->vocab);
         uint64_t bw = 0, bn = 0;
         const double run_start = wall_seconds();
+        const bool guard = cfg.divergence_guard != 0 && !x->deterministic;
         for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
-            sh.reserved.store(x->words_trained);
             const double t0 = wall_seconds();
             PassOut o;
-            run_pass(x, corpus, spans, epoch, sh, &o);
+            for (int attempt = 0;; ++attempt) {
+                const uint64_t words0 = x->words_trained;
+                if (guard) guard_save(x);
+                sh.reserved.store(x->words_trained);
+                o = PassOut{};
+                run_pass(x, corpus, spans, epoch, sh, &o);
+                if (!guard || guard_finite(x)) break;
+                // Hogwild diverged (too many sentences in flight for this
+                // vocabulary and learning rate): restore the epoch's start, halve
+                // the in-flight budget and train the epoch again (same batches).
+                if (attempt == kGuardRetries)
+                    fail(FW2V_ERR_DIVERGED, "Hogwild training diverged (non-finite model) at every in-flight budget tried; "
+                                            "set max_inflight lower or train with deterministic = 1");
+                guard_restore(x);
+                x->words_trained = words0;
+                guard_halve_inflight(x);
+                ++rep.guard_retries;
+                std::fprintf(stderr, "[fw2v] epoch %d: non-finite model, restored; in-flight budget -> %lld sentences\n",
+                             epoch, static_cast<long long>(x->inflight_total));
+            }
             const double secs = wall_seconds() - t0;
             accumulate(rep, o);
             bw += o.batch_words;

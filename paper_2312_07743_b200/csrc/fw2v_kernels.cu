@@ -611,6 +611,23 @@ cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t 
     return cudaGetLastError();
 }
 
+// Divergence guard: *flag |= 1 if any of the n floats at p is not finite
+// (one read of the matrix; 16-byte loads, grid sized to the SMs).
+__global__ void k_nonfinite(const float4* __restrict__ p, size_t n4, int* flag) {
+    bool bad = false;
+    for (size_t x = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; x < n4;
+         x += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float4 v = __ldcg(p + x);
+        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+cudaError_t launch_nonfinite(const float* p, size_t n, int* flag, cudaStream_t st) {
+    if (n % 4 != 0) return cudaErrorInvalidValue;  // rows are padded to a multiple of 4 floats
+    k_nonfinite<<<148 * 4, 256, 0, st>>>(reinterpret_cast<const float4*>(p), n / 4, flag);
+    return cudaGetLastError();
+}
+
 // Hot-row replicas (ModelView::hot): broadcast output rows 0..K-1 into every
 // replica before a Hogwild pass, and average the replicas back after it.
 __global__ void k_hot_broadcast(ModelView m) {

@@ -890,6 +890,12 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
     }
 }
 
+} // namespace fw2v
+
+#include "fw2v_stair.cuh"
+
+namespace fw2v {
+
 // ------------------------------------------------------------------ dispatch
 template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING, bool LIFETIME>
 cudaError_t launch_k1s_inst(int blocks, const ModelView& m, const BatchView& b, int n_neg, DevCounters* ctr,
@@ -945,6 +951,12 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
         if (n_neg + 1 < NC)
             return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
                             : launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
+        // Lifetime order, N = 5, Hogwild overwrite, fast sigmoid: the window staircase.
+        // (W_f <= 3: wider windows spill with both windows' rows live.)
+        if constexpr (NC == 6 && (LANES == 16 || LANES == 32) && WF <= 3 && (VEC == 4 || VEC == 8 || VEC == 10)) {
+            if (lifetime && fast && (m.flags & kFlagNoRing) != 0 && (m.flags & kFlagNoStair) == 0)
+                return launch_k1s_stair<LANES, VEC, WF, true>(m, b, ctr, st, resident);
+        }
         return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
                         : launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
     }

@@ -1,0 +1,414 @@
+// K1s lifetime order as a staircase of windows (sm_100a, CUDA cores).
+//
+// The reference's default update order (sweep_samples, trainer.cpp:133-154:
+// samples outer, contexts inner, every pairing sees the previous pairings'
+// updates) makes pairing (k, j) of a window depend on (k, j-1) and (k-1, j):
+// one window is a wavefront of NC + 2W_f - 1 anti-diagonal steps. Across
+// windows the only dependency (besides sample ids repeated between windows)
+// is that window i+1's first sample may touch context row p only after window
+// i's last sample is done with it: (i+1, 0, j) after (i, NC-1, j+1). Window
+// i+1 can therefore start NC + 1 steps after window i instead of NC + 2W_f - 1:
+// iteration i runs window i's steps 0..NC (the head) interleaved with window
+// i-1's remaining steps (the tail). At W_f = 3, NC = 6 that is 7 steps per
+// window instead of 11, each with 5-6 independent dots (36 per window), and at
+// most 6 sample rows live in registers at any step.
+//
+// Pairings of one step touch disjoint rows (head rows k <= t, tail rows
+// k >= t + 2; context rows of the two windows never coincide in one step), so
+// per sentence the result is the reference order exactly (same FP operations
+// as the one-window wavefront of k1s_snapshot<..., LIFETIME = true>).
+//
+// Windows whose sample ids repeat (inside the window, or shared with the
+// previous window: the reference re-reads the row after the earlier write,
+// trainer.cpp:143) are not overlapped: the pending tail finishes alone, the
+// window's rows are re-read, and a repeat inside the window runs the samples
+// serially with the rewritten row forwarded.
+//
+// Registers: rows Q[r] = syn0 row of position i - W_f + r (r = 0..2W_f; r = W_f
+// is the window's target word, the others its contexts), the head's sample
+// rows Sc, the tail's Sp, and the incoming row. Context rows leave by overwrite
+// (Hogwild, the reference's memcpy write-back, trainer.cpp:61-63); sample rows
+// leave as red.global.add(final - staged) (row += delta).
+#pragma once
+
+namespace fw2v {
+
+template <int LANES, int VEC, int WF>
+struct StairCfg {
+    static constexpr int NC = 6;                       // samples per window (N = 5)
+    static constexpr int NCTX = 2 * WF;
+    static constexpr int NQ = 2 * WF + 1;              // ring rows in registers
+    static constexpr int OFF = NC + 1;                 // window-to-window offset in steps
+    static constexpr int STEPS = NC + NCTX - 1;        // one window's wavefront
+    static constexpr int T = STEPS > OFF ? STEPS - OFF : 0;  // tail steps run in the next iteration
+    static constexpr int STRIDE = LANES * VEC;
+    static constexpr int THREADS = VEC >= 8 ? 64 : kK1Threads;
+    // Staging, double-buffered by window parity, plus the incoming ring row
+    // (16-byte chunks: cp.async.cg, coherent with this thread's st.global.cg).
+    static constexpr int kGroupFloats = (2 * NC + 1) * STRIDE;
+    static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
+    static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
+    static constexpr int kRegBlocks = VEC < 8 ? 3 : 4;
+    static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
+};
+
+// LANES in {16, 32} (a group is half a warp or a warp; the repeat check uses
+// lanes 0..5 and HALF..HALF+5 of the group), N = 5, Hogwild overwrite of the
+// context rows.
+template <int LANES, int VEC, int WF, bool FAST>
+__global__ void __launch_bounds__(StairCfg<LANES, VEC, WF>::THREADS, StairCfg<LANES, VEC, WF>::MINB)
+k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
+    using CF = StairCfg<LANES, VEC, WF>;
+    constexpr int NC = CF::NC, NN = NC - 1, NCTX = CF::NCTX, NQ = CF::NQ, OFF = CF::OFF, T = CF::T;
+    constexpr int H2 = VEC / 2;
+    constexpr int STRIDE = CF::STRIDE;
+    constexpr int HALF = LANES / 2;
+    static_assert(LANES <= 32 && HALF >= NC, "repeat check needs 2 x NC lanes per group");
+    static_assert(VEC % 2 == 0, "8- or 16-byte chunks");
+    using SL = Slice<H2, LANES>;
+    extern __shared__ __align__(16) float k1s_sh[];
+
+    const int lane = threadIdx.x & 31;
+    const int sub = static_cast<int>(threadIdx.x) & (LANES - 1);
+    const int grp = lane / LANES;
+    const int sent = static_cast<int>((blockIdx.x * CF::THREADS + threadIdx.x) / LANES);
+    const bool has = sent < b.n_sentences;
+    float* sbuf = k1s_sh + (threadIdx.x / LANES) * CF::kGroupFloats + sub * SL::CW;  // + (parity*NC + k)*STRIDE
+
+    uint32_t beg = 0, len = 0;
+    float alpha = 0.0f;
+    if (has) {
+        beg = __ldg(b.offsets + sent);
+        len = __ldg(b.offsets + sent + 1) - beg;
+        alpha = __ldg(b.alpha + sent);
+    }
+    const int L = static_cast<int>(len);
+    const int Lmax = static_cast<int>(__reduce_max_sync(kFull, len));
+    if (Lmax == 0) return;
+    const int32_t* __restrict__ ids = b.ids + beg;
+    const int32_t* __restrict__ negs = b.negs + static_cast<size_t>(beg) * NN;
+    float* __restrict__ syn0 = m.syn0 + sub * SL::CW;
+    float* __restrict__ syn1 = m.syn1 + sub * SL::CW;
+    const int hot_k = m.hot_k;
+    const int hot_off = m.hot_k > 0 ? m.hot_row + (sent % m.hot_r) * m.hot_k : 0;
+    auto srow = [&](int s) { return syn1 + static_cast<int64_t>(s < hot_k ? s + hot_off : s) * STRIDE; };
+    const float nha = -0.5f * alpha;
+
+    // Ring rows: Q[r] = position i - WF + r of window i.
+    float2 Q[NQ][H2];
+    int qtok[NQ];
+#pragma unroll
+    for (int r = 0; r < NQ; ++r) {
+        const int p = r - WF;
+        qtok[r] = (p >= 0 && p < L) ? __ldg(ids + p) : -1;
+        if (qtok[r] >= 0) SL::load(Q[r], syn0 + static_cast<int64_t>(qtok[r]) * STRIDE); else vzero2(Q[r]);
+    }
+    unsigned qv = 0;  // bit r: Q[r] holds a position of the sentence
+#pragma unroll
+    for (int r = 0; r < NQ; ++r) qv |= (qtok[r] >= 0 ? 1u : 0u) << r;
+    unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
+    unsigned s_rw = 0, pairs = 0;
+
+    // Sample ids, one per lane: lane q (q = sub mod HALF < NC) of a group holds
+    // sample q of a window (the target id for q = 0, negative q-1 otherwise),
+    // other lanes a unique negative value. idp / idc: windows i-1 / i; idn:
+    // window i+1 (from step T on). Lanes fetch a window's ids by shuffle.
+    const int qid = sub & (HALF - 1);
+    const int qneg = min(max(qid - 1, 0), NN - 1);
+    const int gl = grp * LANES;  // the group's first lane
+    auto make_id = [&](int tok0, int neg, bool active) { return (active && qid < NC) ? (qid == 0 ? tok0 : neg) : -1 - lane; };
+    int idc = make_id(qtok[WF], L >= 2 ? __ldg(negs + qneg) : -1, L >= 2);
+    int idp = -1 - lane, idn = -1 - lane;
+    int nr_next = 1 < L ? __ldg(negs + NN + qneg) : -1;  // this lane's negative of window i+1
+    int tok_ahead = WF + 1 < L ? __ldg(ids + WF + 1) : -1;  // incoming position of window 0
+
+#pragma unroll
+    for (int q = 0; q < 2 * NC + 1; ++q) SL::zero_shared(sbuf + q * STRIDE);
+    const bool l1_exact = (m.flags & kFlagL1Exact) != 0;
+    const int inval_log2 = (m.flags >> kFlagInvalShift) & 15;
+    const unsigned inval_mask = inval_log2 ? (1u << inval_log2) - 1u : 0u;
+
+    // Stage the sample rows of a window (ids in idw) into a buffer.
+    auto prefetch = [&](int idw, int parity) {
+        float* dst = sbuf + parity * NC * STRIDE;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const int s = __shfl_sync(kFull, idw, gl + q);
+            if (s >= 0) SL::stage(dst + q * STRIDE, srow(s));
+        }
+        cp_async_commit();
+    };
+    // Repeats of a window (ids idw): inside the window (dup), or shared with the
+    // previous window (ids idv; lanes HALF.. of the group carry them to the match).
+    auto repeats = [&](int idw, int idv, bool& dup) {
+        const unsigned mm = __match_any_sync(kFull, sub < HALF ? idw : idv);
+        const unsigned lower = ((1u << HALF) - 1u) << gl;
+        const unsigned upper = lower << HALF;
+        dup = __any_sync(kFull, sub < HALF && __popc(mm & lower) > 1);
+        return __any_sync(kFull, sub < HALF && (mm & upper) != 0u);
+    };
+
+    prefetch(idc, 0);
+    bool dup_n = false;
+    bool stale_n = repeats(idc, -1 - lane, dup_n);  // window 0 (no previous window: never stale)
+
+    auto dot = [&](const float2 (&c)[H2], const float2 (&s)[H2]) {
+        float2 acc = __fmul2_rn(c[0], s[0]);
+#pragma unroll
+        for (int h = 1; h < H2; ++h) acc = __ffma2_rn(c[h], s[h], acc);
+        return acc.x + acc.y;
+    };
+    auto update = [&](float2 (&c)[H2], float2 (&s)[H2], float g) {  // pairing_update (kernels.hpp:26-33)
+        const float2 gg = make_float2(g, g);
+#pragma unroll
+        for (int h = 0; h < H2; ++h) {
+            const float2 cc = c[h];
+            c[h] = __ffma2_rn(gg, s[h], cc);
+            s[h] = __ffma2_rn(gg, cc, s[h]);
+        }
+    };
+    // g for a pairing with coefficient hn = valid ? -alpha/2 : 0 (label 1 for k = 0).
+    auto coeff = [&](float f, float hn, bool positive) {
+        if constexpr (FAST) {
+            const float h = fminf(fmaxf(0.5f * f, -3.0f), 3.0f);
+            return fmaf(hn, tanh_approx(h), positive ? -hn : hn);
+        } else {
+            return sgd_coeff<false>(f, positive ? 1.0f : 0.0f, -2.0f * hn);
+        }
+    };
+    auto writeback = [&](const float2 (&s)[H2], const float* staged, int sid, bool pred) {
+        float2 e[H2];
+        SL::load_shared(e, staged);
+#pragma unroll
+        for (int h = 0; h < H2; ++h) e[h] = make_float2(s[h].x - e[h].x, s[h].y - e[h].y);
+        SL::red_add_if(pred && sid >= 0, srow(max(sid, 0)), e);
+    };
+    // Context slot j of the current window -> ring row; of the previous window -> ring row.
+    auto rh = [](int j) { return j < WF ? j : j + 1; };
+    auto rt = [](int j) { return j < WF ? j - 1 : j; };
+
+    float2 Sc[NC][H2], Sp[NC][H2];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) { vzero2(Sc[k]); vzero2(Sp[k]); }
+    bool tact = false;  // the previous window's tail is pending
+    unsigned tvm = 0;   // tail validity per ring row (previous window, current indexing)
+
+    // One step t of iteration i: head pairings (k, t-k) of window i, tail
+    // pairings (k, t+OFF-k) of window i-1.
+    // (t and HEAD are constants once the step loops below are unrolled.)
+    auto step = [&](const int t, const bool HEAD, unsigned hvm, const float* cur, const float* prv, bool wact) {
+        float f[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            const int jh = t - k, jt = t + OFF - k;
+            if (HEAD && jh >= 0 && jh < NCTX) f[k] = dot(Q[rh(jh)], Sc[k]);
+            else if (jt >= 0 && jt < NCTX) f[k] = dot(Q[rt(jt)], Sp[k]);
+        }
+#pragma unroll
+        for (int o = LANES / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                const int jh = t - k, jt = t + OFF - k;
+                if ((HEAD && jh >= 0 && jh < NCTX) || (jt >= 0 && jt < NCTX)) f[k] += __shfl_xor_sync(kFull, f[k], o);
+            }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            const int jh = t - k, jt = t + OFF - k;
+            if (HEAD && jh >= 0 && jh < NCTX) {
+                update(Q[rh(jh)], Sc[k], coeff(f[k], ((hvm >> rh(jh)) & 1u) ? nha : 0.0f, k == 0));
+                if (jh == NCTX - 1) writeback(Sc[k], cur + k * STRIDE, __shfl_sync(kFull, idc, gl + k), wact);
+            } else if (jt >= 0 && jt < NCTX) {
+                update(Q[rt(jt)], Sp[k], coeff(f[k], ((tvm >> rt(jt)) & 1u) ? nha : 0.0f, k == 0));
+                if (jt == NCTX - 1) writeback(Sp[k], prv + k * STRIDE, __shfl_sync(kFull, idp, gl + k), tact);
+            }
+        }
+    };
+
+    for (int i = 0; i < Lmax; ++i) {
+        const bool act = i < L;
+        const bool wact = act && L >= 2;
+        const int q_in = i + 1 + WF;
+        const float* cur = sbuf + (i & 1) * NC * STRIDE;
+        const float* prv = sbuf + ((i + 1) & 1) * NC * STRIDE;
+        // Early loads: the incoming ring row (position i+1+W_f), the next ids,
+        // window i+2's negatives; L2 prefetch of the id/negative streams.
+        const int inc_tok = tok_ahead;
+        constexpr bool kIncSmem = SL::CW == 4;
+        float2 inc[H2];
+        if constexpr (!kIncSmem) SL::load_early(inc, syn0 + static_cast<int64_t>(max(inc_tok, 0)) * STRIDE);
+        const int last = max(L - 1, 0);
+        const int tok_raw = ldg_early(ids + min(q_in + 1, last));
+        const int nr_raw = ldg_early(negs + static_cast<size_t>(min(i + 2, last)) * NN + qneg);
+        const bool tok_ok = q_in + 1 < L;
+        if (sub == 0 && i + kPrefetchWindows < L) {
+            prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * NN);
+            prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
+        }
+        c_reads += inc_tok >= 0;
+
+        const unsigned hvm = wact ? qv : 0u;  // head validity per ring row
+
+        const bool dup = dup_n;
+        if (stale_n || dup) {
+            // Not overlapped: the previous window's tail alone, then this
+            // window's rows re-read after its write-backs. (Warp-uniform branch:
+            // the steps shuffle; a sentence without a pending tail has tvm = 0.)
+            if (__any_sync(kFull, tact)) {
+#pragma unroll
+                for (int t = 0; t < T; ++t) step(t, false, 0u, cur, prv, wact);
+                tact = false;
+                tvm = 0;
+            }
+            cp_async_wait_group<0>();
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                float2 v[H2];
+                SL::load(v, srow(max(__shfl_sync(kFull, idc, gl + q), 0)));
+                SL::store_shared(const_cast<float*>(cur) + q * STRIDE, v);
+            }
+        } else {
+            cp_async_wait_group<0>();
+        }
+        float* inc_sh = sbuf + 2 * NC * STRIDE;
+        if constexpr (kIncSmem) {
+            if (inc_tok >= 0) {
+                const float* src = syn0 + static_cast<int64_t>(inc_tok) * STRIDE;
+#pragma unroll
+                for (int c = 0; c < SL::NCH; ++c) {
+                    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(inc_sh + c * SL::CS));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * SL::CS) : "memory");
+                }
+            }
+            cp_async_commit();
+        }
+        // (Next window's staging is issued after this window's tail steps.)
+        auto issue_next = [&]() {
+            if (l1_exact || (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
+                             (threadIdx.x >> 5) == 0))
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            const bool nact = i + 1 < L && L >= 2;
+            idn = make_id(qtok[WF + 1], nr_next, nact);
+            if (i + 1 < Lmax) prefetch(idn, (i + 1) & 1);
+            else cp_async_commit();  // the slide below waits for all but the newest group
+            stale_n = repeats(idn, idc, dup_n);
+        };
+        if (!dup) {
+            // Sample rows enter one step before their first pairing.
+            SL::load_shared(Sc[0], cur);
+#pragma unroll
+            for (int t = 0; t < OFF; ++t) {
+                if (t + 1 < NC) SL::load_shared(Sc[t + 1], cur + (t + 1) * STRIDE);
+                step(t, true, hvm, cur, prv, wact);
+                if (t == T) issue_next();
+            }
+            // Rows k >= OFF - NCTX + 1 finish in the next iteration's tail.
+#pragma unroll
+            for (int k = 0; k < NC; ++k) vcopy2(Sp[k], Sc[k]);
+            tvm = hvm;
+            tact = wact && T > 0;
+        } else {
+            // Reference order, sample by sample; a repeated id starts from the
+            // row its previous occurrence left (the reference re-reads it).
+            int sidc[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) sidc[k] = __shfl_sync(kFull, idc, gl + k);
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                SL::load_shared(Sc[k], cur + k * STRIDE);
+#pragma unroll
+                for (int k2 = 0; k2 < k; ++k2)
+                    if (sidc[k2] == sidc[k]) vcopy2(Sc[k], Sc[k2]);
+#pragma unroll
+                for (int j = 0; j < NCTX; ++j) {
+                    float f = dot(Q[rh(j)], Sc[k]);
+#pragma unroll
+                    for (int o = LANES / 2; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
+                    update(Q[rh(j)], Sc[k], coeff(f, ((hvm >> rh(j)) & 1u) ? nha : 0.0f, k == 0));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                bool last_occ = true;
+#pragma unroll
+                for (int q2 = q + 1; q2 < NC; ++q2) last_occ &= sidc[q2] != sidc[q];
+                writeback(Sc[q], cur + q * STRIDE, sidc[q], wact && last_occ);
+            }
+            issue_next();
+            tact = false;
+            tvm = 0;
+        }
+        if (wact) {
+            s_rw += NC;
+            pairs += static_cast<unsigned>(__popc(qv & ~(1u << WF))) * NC;
+        }
+
+        // Slide the ring (ContextRing::advance, trainer.cpp:55-69): position
+        // i - W_f leaves (its last pairing was window i's), i+1+W_f enters.
+        if constexpr (kIncSmem) {
+            cp_async_wait_group<1>();
+            SL::load_shared(inc, inc_sh);
+        }
+        if (qtok[0] >= 0) {
+            SL::store(syn0 + static_cast<int64_t>(qtok[0]) * STRIDE, Q[0]);
+            if (inc_tok == qtok[0]) vcopy2(inc, Q[0]);
+        }
+#pragma unroll
+        for (int r = 0; r < NQ - 1; ++r) { vcopy2(Q[r], Q[r + 1]); qtok[r] = qtok[r + 1]; }
+        vcopy2(Q[NQ - 1], inc);
+        qtok[NQ - 1] = inc_tok;
+        tvm >>= 1;
+        qv = (qv >> 1) | ((inc_tok >= 0 ? 1u : 0u) << (NQ - 1));
+        idp = idc;
+        idc = idn;
+        nr_next = i + 2 < L ? nr_raw : -1;
+        tok_ahead = tok_ok ? tok_raw : -1;
+    }
+    // The last window's tail.
+    if (__any_sync(kFull, tact)) {
+        const float* prv = sbuf + ((Lmax + 1) & 1) * NC * STRIDE;
+#pragma unroll
+        for (int t = 0; t < T; ++t) step(t, false, 0u, prv, prv, false);
+    }
+    // ContextRing::finish (trainer.cpp:71-75): the residents, in any order (overwrite).
+#pragma unroll
+    for (int r = 0; r < NQ; ++r)
+        if (qtok[r] >= 0) SL::store(syn0 + static_cast<int64_t>(qtok[r]) * STRIDE, Q[r]);
+
+    if (ctr != nullptr) {
+        const bool lead = has && sub == 0;
+        const unsigned hits = (L >= 2) ? pairs - static_cast<unsigned>(L) : 0u;
+        const unsigned v0 = __reduce_add_sync(kFull, lead ? c_reads : 0u);
+        const unsigned v2 = __reduce_add_sync(kFull, lead ? s_rw : 0u);
+        const unsigned v4 = __reduce_add_sync(kFull, lead ? hits : 0u);
+        const unsigned v5 = __reduce_add_sync(kFull, lead ? static_cast<unsigned>(L) : 0u);
+        const unsigned v6 = __reduce_add_sync(kFull, lead ? 1u : 0u);
+        if (lane == 0) {
+            atomicAdd(&ctr->context_reads, v0);
+            atomicAdd(&ctr->context_writes, v5);
+            atomicAdd(&ctr->sample_reads, v2);
+            atomicAdd(&ctr->sample_writes, v2);
+            atomicAdd(&ctr->ring_hits, v4);
+            atomicAdd(&ctr->words, v5);
+            atomicAdd(&ctr->sentences, v6);
+        }
+    }
+}
+
+template <int LANES, int VEC, int WF, bool FAST>
+cudaError_t launch_k1s_stair(const ModelView& m, const BatchView& b, DevCounters* ctr, cudaStream_t st, int* resident) {
+    using CF = StairCfg<LANES, VEC, WF>;
+    constexpr int bytes = CF::kBlockBytes;
+    auto* kern = k1s_stair<LANES, VEC, WF, FAST>;
+    static std::atomic<uint64_t> configured{0};
+    if (cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), bytes, configured); e != cudaSuccess)
+        return e;
+    constexpr int threads = CF::THREADS;
+    if (resident != nullptr) return resident_sentences(kern, bytes, threads, threads / LANES, resident);
+    const int per_block = threads / LANES;
+    const int blocks = (b.n_sentences + per_block - 1) / per_block;
+    if (blocks == 0) return cudaSuccess;
+    kern<<<blocks, threads, bytes, st>>>(m, b, ctr);
+    return cudaGetLastError();
+}
+
+} // namespace fw2v

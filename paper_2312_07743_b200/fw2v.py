@@ -70,6 +70,7 @@ class CConfig(C.Structure):
         ("fast_sigmoid", C.c_int32), ("k1_lanes", C.c_int32), ("streams", C.c_int32),
         ("l1_refresh_log2", C.c_int32), ("delta_writeback", C.c_int32), ("max_inflight", C.c_int32),
         ("hot_rows", C.c_int32), ("hot_replicas", C.c_int32), ("replica_merge", C.c_int32),
+        ("divergence_guard", C.c_int32),
     ]
 
 
@@ -92,7 +93,7 @@ class CReport(C.Structure):
         ("words_trained", C.c_uint64), ("sentences_trained", C.c_uint64), ("vocab_size", C.c_uint64),
         ("wall_seconds", C.c_double), ("batching_words_per_sec", C.c_double), ("n_epochs", C.c_int32),
         ("traffic", CCounters), ("analytic", CCounters), ("kernel_seconds", C.c_double),
-        ("h2d_bytes", C.c_uint64),
+        ("h2d_bytes", C.c_uint64), ("guard_retries", C.c_int32),
     ]
 
 
@@ -135,6 +136,7 @@ class TrainConfig:
     hot_rows: int = 64
     hot_replicas: int = 16
     replica_merge: str = "touched"  # data-parallel rounds: mean | touched (include/fw2v.h)
+    divergence_guard: int = 1  # Hogwild: finite check per epoch, restore + halve in-flight on failure
 
     @property
     def context_width(self) -> int:
@@ -167,6 +169,7 @@ class Report:
     h2d_bytes: int
     epochs: list = field(default_factory=list)
     kernel_seconds: float = 0.0
+    guard_retries: int = 0
 
 
 _lib = None
@@ -489,7 +492,8 @@ class Trainer:
 
 def _report(rep, epochs) -> Report:
     return Report(rep.words_trained, rep.sentences_trained, rep.wall_seconds, rep.batching_words_per_sec,
-                  rep.traffic.as_tuple(), rep.analytic.as_tuple(), rep.h2d_bytes, epochs, rep.kernel_seconds)
+                  rep.traffic.as_tuple(), rep.analytic.as_tuple(), rep.h2d_bytes, epochs, rep.kernel_seconds,
+                  rep.guard_retries)
 
 
 def _handles(trainers):

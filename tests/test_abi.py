@@ -44,6 +44,19 @@ def test_config_defaults_mirror_trainconfig(oracle):
     assert c.alpha0 == pytest.approx(0.025) and c.subsample == 1e-4 and c.table_power == 0.75
 
 
+def test_extension_defaults_mirror_python():
+    """The C defaults of the B200 extension fields equal the Python dataclass's
+    (TrainConfig.to_c writes every field, so the two must not drift)."""
+    c = fw.fw2v.CConfig()
+    fw.fw2v.lib().fw2v_config_default(ctypes.byref(c))
+    py = fw.TrainConfig().to_c()
+    for name, _ in fw.fw2v.CConfig._fields_:
+        if name in ("workers",):
+            continue
+        assert getattr(c, name) == getattr(py, name), name
+    assert c.divergence_guard == 1
+
+
 def test_validate_config_rejects_like_reference():
     bad = fw.fw2v.CConfig()
     fw.fw2v.lib().fw2v_config_default(ctypes.byref(bad))

@@ -1,0 +1,65 @@
+"""Divergence guard (fw2v_config.divergence_guard, csrc/fw2v_host.cpp): after
+each Hogwild epoch the model is checked for non-finite values; a diverged
+epoch is restored from its HBM snapshot and trained again with half the
+in-flight budget, up to 4 times, then FW2V_ERR_DIVERGED. The reference has no
+such failure mode (16 CPU threads); thousands of GPU sentences in flight do
+(DESIGN.md §5)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+fw = pytest.importorskip("paper_2312_07743_b200")
+
+
+@pytest.fixture(scope="module")
+def text8():
+    return fw.synth_zipf(**fw.TEXT8_SHAPE).head(6000)
+
+
+def _cfg(**kw):
+    base = dict(dim=128, window=5, negatives=5, epochs=2, workers=16, streams=4, deterministic=0, sampler="alias",
+                reuse_mode="window_snapshot", hot_rows=0, max_inflight=-1, seed=5)
+    base.update(kw)
+    return fw.TrainConfig(**base)
+
+
+def test_guard_unreachable_rate_fails_loudly(text8):
+    """alpha0 = 40 diverges at every budget: the call fails with
+    FW2V_ERR_DIVERGED instead of returning a non-finite model."""
+    with fw.Trainer(_cfg(alpha0=40.0, epochs=1), text8.counts) as t:
+        with pytest.raises(fw.Fw2vError) as e:
+            t.train_corpus(text8)
+        assert e.value.code == 67
+
+
+def test_guard_restores_and_retrains(text8):
+    """A rate that diverges with every sentence of a batch in flight but trains
+    with fewer: the guard retries and the model stays finite; without the guard
+    the same run is non-finite."""
+    for alpha0 in (1.0, 2.0, 4.0):
+        with fw.Trainer(_cfg(alpha0=alpha0, divergence_guard=0), text8.counts) as t:
+            t.train_corpus(text8)
+            gi, go = t.get_model()
+        if not (np.isfinite(gi).all() and np.isfinite(go).all()):
+            break
+    else:
+        pytest.skip("no tested rate diverges uncapped")
+    with fw.Trainer(_cfg(alpha0=alpha0), text8.counts) as t:
+        try:
+            rep = t.train_corpus(text8)
+        except fw.Fw2vError as e:
+            assert e.code == 67
+            pytest.skip(f"alpha0={alpha0} diverges at every budget")
+        gi, go = t.get_model()
+    print(f"alpha0={alpha0}: guard retries {rep.guard_retries}")
+    assert rep.guard_retries >= 1
+    assert np.isfinite(gi).all() and np.isfinite(go).all()
+    assert rep.words_trained > 0
+
+
+def test_guard_quiet_at_the_bench_rate(text8):
+    """At the bench's rate the guard never fires and the result equals the
+    unguarded run's word count."""
+    with fw.Trainer(_cfg(alpha0=0.025, max_inflight=0), text8.counts) as t:
+        rep = t.train_corpus(text8)
+    assert rep.guard_retries == 0

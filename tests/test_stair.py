@@ -1,0 +1,107 @@
+"""Lifetime order as a window staircase (csrc/fw2v_stair.cuh) vs the
+one-window wavefront (k1s_snapshot<..., LIFETIME = true>, FW2V_NO_STAIR=1).
+
+Both run the reference's sweep_samples order (trainer.cpp:133-154) with the
+same FP operations per pairing, so on launches whose sentences cannot interact
+(disjoint id ranges for rows and negatives) the two kernels must agree bit for
+bit — including sentences of unequal length sharing a warp, windows with
+repeated sample ids (serial fallback) and ids shared between consecutive
+windows (tail finished before the window starts). Against the oracle the
+staircase is covered by tests/test_parity_bench.py (lifetime, bench knobs).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import sgns_loss
+
+pytestmark = pytest.mark.gpu
+fw = pytest.importorskip("paper_2312_07743_b200")
+
+
+def _run(stair, cfg, counts, inp, out, launches):
+    old = os.environ.pop("FW2V_NO_STAIR", None)
+    if not stair:
+        os.environ["FW2V_NO_STAIR"] = "1"
+    try:
+        with fw.Trainer(cfg, counts) as t:
+            t.set_model(inp, out)
+            ctrs = []
+            for offsets, ids, negs, alphas in launches:
+                ctrs.append(t.train_sentences(offsets, ids, negs, alphas, serial=False).as_tuple())
+            gi, go = t.get_model()
+    finally:
+        os.environ.pop("FW2V_NO_STAIR", None)
+        if old is not None:
+            os.environ["FW2V_NO_STAIR"] = old
+    return gi, go, ctrs
+
+
+def _disjoint_launch(rng, n_sent, band, lens, n_neg, types_per_band):
+    """n_sent sentences, sentence s drawing ids and negatives only from band s
+    (ids s*band .. s*band + types_per_band - 1): no row is shared between sentences."""
+    ids, negs, offs = [], [], [0]
+    for s in range(n_sent):
+        L = int(lens[s])
+        lo = s * band
+        ids.append(rng.integers(lo, lo + types_per_band, L))
+        negs.append(rng.integers(lo, lo + types_per_band, L * n_neg))
+        offs.append(offs[-1] + L)
+    alphas = rng.uniform(0.005, 0.05, n_sent).astype(np.float32)
+    return (np.array(offs, np.uint64), np.concatenate(ids).astype(np.int32),
+            np.concatenate(negs).astype(np.int32), alphas)
+
+
+@pytest.mark.parametrize("dim", [64, 128, 256, 300])
+@pytest.mark.parametrize("window", [2, 4, 5, 6])
+@pytest.mark.parametrize("types_per_band", [7, 40, 500], ids=["repeats", "some", "rare"])
+def test_stair_equals_wavefront_bitwise(dim, window, types_per_band):
+    n_neg = 5
+    rng = np.random.default_rng(dim * 100 + window * 10 + types_per_band)
+    n_sent, band = 24, 600
+    V = n_sent * band
+    counts = (10 + V - np.arange(V)).astype(np.uint64)
+    launches = []
+    for _ in range(3):
+        lens = rng.integers(1, 90, n_sent)
+        lens[:4] = [1, 2, 3, 2 * window + 3][:4]  # edge lengths share warps with long sentences
+        launches.append(_disjoint_launch(rng, n_sent, band, lens, n_neg, types_per_band))
+    inp = ((rng.random((V, dim)) - 0.5) / dim).astype(np.float32)
+    out = ((rng.random((V, dim)) - 0.5) * 0.5).astype(np.float32)
+    cfg = fw.TrainConfig(dim=dim, window=window, negatives=n_neg, workers=4, deterministic=0,
+                         reuse_mode="lifetime", fast_sigmoid=True, delta_writeback=2, l1_refresh_log2=0,
+                         hot_rows=0)
+    a_in, a_out, a_ctr = _run(True, cfg, counts, inp, out, launches)
+    b_in, b_out, b_ctr = _run(False, cfg, counts, inp, out, launches)
+    assert a_ctr == b_ctr
+    assert np.isfinite(a_in).all() and np.isfinite(a_out).all()
+    assert not np.array_equal(a_out, out), "nothing trained"
+    assert np.array_equal(a_in, b_in), np.abs(a_in - b_in).max()
+    assert np.array_equal(a_out, b_out), np.abs(a_out - b_out).max()
+
+
+@pytest.mark.parametrize("hot_rows", [0, 64])
+def test_stair_hogwild_text8_loss(hot_rows):
+    """A Hogwild epoch on the text8 shape: the staircase and the wavefront reach
+    the same SGNS loss (they differ only in Hogwild interleaving)."""
+    corpus = fw.synth_zipf(**fw.TEXT8_SHAPE).head(4000)
+    cfg = fw.TrainConfig(dim=128, window=5, negatives=5, epochs=1, workers=16, streams=4, deterministic=0,
+                         reuse_mode="lifetime", sampler="alias", hot_rows=hot_rows, seed=3)
+    losses = []
+    for stair in (True, False):
+        old = os.environ.pop("FW2V_NO_STAIR", None)
+        if not stair:
+            os.environ["FW2V_NO_STAIR"] = "1"
+        try:
+            with fw.Trainer(cfg, corpus.counts) as t:
+                t.train_corpus(corpus)
+                gi, go = t.get_model()
+        finally:
+            os.environ.pop("FW2V_NO_STAIR", None)
+            if old is not None:
+                os.environ["FW2V_NO_STAIR"] = old
+        negs = np.random.default_rng(0).integers(0, len(corpus.counts), len(corpus.ids) * 5).astype(np.int32)
+        losses.append(sgns_loss(gi, go, corpus.offsets, corpus.ids, negs, 3, 5))
+    print("loss stair / wavefront", losses)
+    assert abs(losses[0] - losses[1]) <= 0.005 * losses[1]
