@@ -300,10 +300,11 @@ def dropin_leg(fw, args, corpus):
         return {"unavailable": str(e)}
     out = {"path": "ringvec::train (C++ drop-in, libringvec_fw2v.so) per call: fw2v_create (tables, HBM model, "
                    "init_model), host batching, H2D, kernels, model readback; reference default TrainConfig "
-                   "(workers=0 -> hardware threads, alias sampler, no hot-row replicas)"}
+                   "(epochs=20, workers=0 -> hardware threads; alias sampler, no hot-row replicas, "
+                   "auto in-flight budget)"}
     try:
         for mode in ("lifetime", "window_snapshot"):
-            cfg = fw.TrainConfig(dim=args.dim, window=args.window, negatives=args.negatives, epochs=1, workers=0,
+            cfg = fw.TrainConfig(dim=args.dim, window=args.window, negatives=args.negatives, epochs=20, workers=0,
                                  batch_sentences=args.batch_sentences, subsample=1e-4, seed=1, reuse_mode=mode)
             h.train(cfg)  # warm-up (first CUDA context, page-in)
             calls = [h.train(cfg) for _ in range(3)]

@@ -158,6 +158,10 @@ int fw2v_device_count(int* count);
  * (trainer.cpp:390-410). */
 int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_size, fw2v_ctx** out);
 void fw2v_destroy(fw2v_ctx* ctx);
+/* Batch-pipeline buffers (pinned host, device) of destroyed contexts are cached
+ * process-wide and reused by the next context (a ringvec::train call creates and
+ * destroys one); this returns the cached ones to the driver. */
+void fw2v_release_cached(void);
 
 /* Model I/O, dense |V| x dim fp32 row-major host arrays (EmbeddingModel,
  * model.hpp:16-42). Either pointer may be NULL. */

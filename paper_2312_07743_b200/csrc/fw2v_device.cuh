@@ -21,6 +21,7 @@ struct BatchView {
     const int32_t* negs;
     const float* alpha;
     int32_t n_sentences;
+    int32_t max_groups = 0;  // K1s: at most this many sentences in flight (grid-stride launch); 0 = all
 };
 
 // Embedding matrices in HBM: row w of syn0 (reference `input`, context side)

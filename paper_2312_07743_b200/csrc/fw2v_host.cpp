@@ -28,6 +28,8 @@
 #include <sys/mman.h>
 #if defined(__x86_64__)
 #include <immintrin.h>
+#include <map>
+#include <unordered_map>
 #endif
 #include <memory>
 #include <mutex>
@@ -559,6 +561,86 @@ void require_device(int device) {
     FW2V_CK(cudaSetDevice(device));
 }
 
+// Process-wide cache of the batch pipeline's pinned host and device buffers.
+// A ringvec::train user creates, trains and destroys a context per call; without
+// the cache every call pays ~0.3 s of cudaHostAlloc for its slots. Freed blocks
+// are kept (up to kPoolCap bytes per kind and device) and handed out again to a
+// request of at most their size and at least half of it. fw2v_release_cached()
+// returns them to the driver.
+class BufferPool {
+public:
+    static BufferPool& get() {
+        static BufferPool* p = new BufferPool();  // never destroyed: no teardown-order issues
+        return *p;
+    }
+    void* host(size_t bytes) { return take(kHost, bytes); }
+    void* device(size_t bytes) {
+        int dev = 0;
+        FW2V_CK(cudaGetDevice(&dev));
+        return take(dev, bytes);
+    }
+    void put(void* p) {
+        if (p == nullptr) return;
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = live_.find(p);
+        if (it == live_.end()) return;
+        const auto [key, bytes] = it->second;
+        live_.erase(it);
+        if (cached_[key] + bytes > kPoolCap) {
+            release_block(key, p);
+            return;
+        }
+        cached_[key] += bytes;
+        free_[key].emplace(bytes, p);
+    }
+    void release_all() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto& [key, m] : free_)
+            for (auto& [bytes, p] : m) release_block(key, p);
+        free_.clear();
+        cached_.clear();
+    }
+
+private:
+    static constexpr int kHost = -1;
+    static constexpr size_t kPoolCap = size_t{16} << 30;
+    void* take(int key, size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto& m = free_[key];
+            auto it = m.lower_bound(bytes);
+            if (it != m.end() && it->first <= 2 * bytes) {
+                void* p = it->second;
+                live_[p] = {key, it->first};
+                cached_[key] -= it->first;
+                m.erase(it);
+                return p;
+            }
+        }
+        void* p = nullptr;
+        if (key == kHost) FW2V_CK(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+        else FW2V_CK(cudaMalloc(&p, bytes));
+        std::lock_guard<std::mutex> lk(mu_);
+        live_[p] = {key, bytes};
+        return p;
+    }
+    static void release_block(int key, void* p) {
+        if (key == kHost) {
+            cudaFreeHost(p);
+        } else {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(key);
+            cudaFree(p);
+            cudaSetDevice(cur);
+        }
+    }
+    std::mutex mu_;
+    std::map<int, std::multimap<size_t, void*>> free_;
+    std::map<int, size_t> cached_;
+    std::unordered_map<void*, std::pair<int, size_t>> live_;
+};
+
 // One producer lane: stream + two double-buffered batch slots.
 struct Slot {
     int32_t* h_ids = nullptr;
@@ -584,8 +666,11 @@ struct Lane {
     void release() {
         for (Slot& s : slot) {
             if (s.h2d_done) cudaEventSynchronize(s.h2d_done);
-            cudaFreeHost(s.h_ids); cudaFreeHost(s.h_off); cudaFreeHost(s.h_negs); cudaFreeHost(s.h_alpha);
-            cudaFree(s.d_ids); cudaFree(s.d_off); cudaFree(s.d_negs); cudaFree(s.d_alpha);
+            BufferPool& pool = BufferPool::get();
+            for (void* p : {static_cast<void*>(s.h_ids), static_cast<void*>(s.h_off), static_cast<void*>(s.h_negs),
+                            static_cast<void*>(s.h_alpha), static_cast<void*>(s.d_ids), static_cast<void*>(s.d_off),
+                            static_cast<void*>(s.d_negs), static_cast<void*>(s.d_alpha)})
+                pool.put(p);
             if (s.h2d_done) cudaEventDestroy(s.h2d_done);
             if (s.used) cudaEventDestroy(s.used);
             s = Slot{};
@@ -705,6 +790,12 @@ struct fw2v_ctx {
 
     cudaError_t launch(const BatchView& bv, bool serial, DevCounters* ctr, cudaStream_t st, int streams = 1) const {
         const int64_t cap = serial ? 0 : inflight_per_stream(streams);
+        if (cap > 0 && bv.n_sentences > cap && k1s_shape.lanes > 0 &&
+            (cfg.reuse_mode == kLifetime || cfg.reuse_mode == kWindowSnapshot)) {
+            BatchView b = bv;  // K1s: one grid-stride launch of at most `cap` sentences in flight
+            b.max_groups = static_cast<int32_t>(cap);
+            return launch_one(b, false, ctr, st);
+        }
         if (cap > 0 && bv.n_sentences > cap) {
             for (int64_t s0 = 0; s0 < bv.n_sentences; s0 += cap) {
                 BatchView sub = bv;
@@ -751,18 +842,19 @@ struct fw2v_ctx {
             if (!ln.d_ctr) FW2V_CK(cudaMalloc(&ln.d_ctr, sizeof(DevCounters)));
             if (ln.cap_words >= cap_words && ln.cap_sent >= cap_sent) continue;
             ln.release();
+            BufferPool& pool = BufferPool::get();
             for (Slot& s : ln.slot) {
-                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_ids), 4 * cap_words, cudaHostAllocDefault));
-                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_negs), 4 * cap_words * nn, cudaHostAllocDefault));
-                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_off), 4 * (cap_sent + 1), cudaHostAllocDefault));
-                FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&s.h_alpha), 4 * cap_sent, cudaHostAllocDefault));
-                FW2V_CK(cudaMalloc(&s.d_ids, 4 * cap_words));
-                FW2V_CK(cudaMalloc(&s.d_negs, 4 * cap_words * nn + kNegPadBytes));
+                s.h_ids = static_cast<int32_t*>(pool.host(4 * cap_words));
+                s.h_negs = static_cast<int32_t*>(pool.host(4 * cap_words * nn));
+                s.h_off = static_cast<uint32_t*>(pool.host(4 * (cap_sent + 1)));
+                s.h_alpha = static_cast<float*>(pool.host(4 * cap_sent));
+                s.d_ids = static_cast<int32_t*>(pool.device(4 * cap_words));
+                s.d_negs = static_cast<int32_t*>(pool.device(4 * cap_words * nn + kNegPadBytes));
                 // K1s reads a window's negatives as one fixed-size group (masked where
                 // consumed), possibly past the copied part: keep it defined.
                 FW2V_CK(cudaMemset(s.d_negs, 0, 4 * cap_words * nn + kNegPadBytes));
-                FW2V_CK(cudaMalloc(&s.d_off, 4 * (cap_sent + 1)));
-                FW2V_CK(cudaMalloc(&s.d_alpha, 4 * cap_sent));
+                s.d_off = static_cast<uint32_t*>(pool.device(4 * (cap_sent + 1)));
+                s.d_alpha = static_cast<float*>(pool.device(4 * cap_sent));
                 FW2V_CK(cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming));
                 FW2V_CK(cudaEventCreateWithFlags(&s.used, cudaEventDisableTiming));
             }
@@ -955,8 +1047,10 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         for (uint64_t c : x->counts) x->total_retained += c;
         x->keep.resize(static_cast<size_t>(vocab_size));
         x->keep_on = keep_probs(counts, vocab_size, cfg->subsample, x->keep.data());
-        x->slots.resize(cfg->table_size);
-        build_table(counts, vocab_size, cfg->table_power, cfg->table_size, x->slots.data());
+        if (!(cfg->sampler == FW2V_SAMPLER_ALIAS && !x->deterministic)) {  // fw2v_ctx::sampler() reads it
+            x->slots.resize(cfg->table_size);
+            build_table(counts, vocab_size, cfg->table_power, cfg->table_size, x->slots.data());
+        }
         if (cfg->sampler == FW2V_SAMPLER_ALIAS) x->alias.build(counts, vocab_size, cfg->table_power);
         require_device(cfg->device);
         const size_t bytes = sizeof(float) * static_cast<size_t>(vocab_size) * static_cast<size_t>(x->stride);
@@ -986,6 +1080,8 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
 }
 
 void fw2v_destroy(fw2v_ctx* ctx) { delete ctx; }
+
+void fw2v_release_cached(void) { BufferPool::get().release_all(); }
 
 int fw2v_init_model(fw2v_ctx* x, uint64_t seed) {
     return guarded([&] {

@@ -276,10 +276,10 @@ constexpr int kFullChunk = 0, kPartChunk = 1, kMultiChunk = 2;
 // steps of up to 6 independent dots (the wavefront), with the sample rows in
 // registers; windows whose sample ids repeat run the samples serially with the
 // rewritten row forwarded (the reference re-reads it, trainer.cpp:143).
+// One sentence per lane group: sentences sent0 + (threadIdx.x / LANES) of the block.
 template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true, bool LIFETIME = false>
-__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == 2 && !LIFETIME>::THREADS,
-                                  K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == 2 && !LIFETIME>::MINB)
-k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ ctr) {
+__device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView& b, int n_neg_arg,
+                                             DevCounters* __restrict__ ctr, int sent0) {
     static_assert(VEC % 2 == 0, "K1s stages 8- or 16-byte chunks");
     constexpr bool MULTI = MODE == kMultiChunk;
     constexpr bool FULL = MODE == kFullChunk;
@@ -311,7 +311,7 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
     const int csub = lane & (CL - 1);                               // control / butterfly lane
     const int grp = lane / CL;
     const int wig = static_cast<int>(threadIdx.x >> 5) & (SM::NWG - 1);  // warp in group
-    const int sent = static_cast<int>((blockIdx.x * SM::THREADS + threadIdx.x) / LANES);
+    const int sent = sent0 + static_cast<int>(threadIdx.x / LANES);
     const bool has = sent < b.n_sentences;
     float* gbase = k1s_sh + (threadIdx.x / LANES) * SM::kGroupFloats;
     float* gsh = gbase + wig * SM::GPAD;
@@ -888,6 +888,25 @@ k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ 
             atomicAdd(&ctr->sentences, v6);
         }
     }
+    cp_async_wait_group<0>();  // the staging buffers are the next sentence's
+}
+
+// Blocks stride over the batch's sentences (BatchView::max_groups caps the grid:
+// the Hogwild in-flight budget without splitting the batch into launches).
+template <int LANES, int VEC, int WF, int NC, int MODE, bool FAST, bool RING = true, bool LIFETIME = false>
+__global__ void __launch_bounds__(K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == 2 && !LIFETIME>::THREADS,
+                                  K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == 2 && !LIFETIME>::MINB)
+k1s_snapshot(ModelView m, BatchView b, int n_neg_arg, DevCounters* __restrict__ ctr) {
+    constexpr int PB = K1sSmem<LANES, VEC, WF, NC, RING, LIFETIME, MODE == 2 && !LIFETIME>::THREADS / LANES;
+    for (int s0 = static_cast<int>(blockIdx.x) * PB; s0 < b.n_sentences; s0 += static_cast<int>(gridDim.x) * PB)
+        k1s_sentence<LANES, VEC, WF, NC, MODE, FAST, RING, LIFETIME>(m, b, n_neg_arg, ctr, s0);
+}
+
+// Grid for a batch, capped by the in-flight budget (BatchView::max_groups).
+inline int k1s_grid(const BatchView& b, int per_block) {
+    int blocks = (b.n_sentences + per_block - 1) / per_block;
+    if (b.max_groups > 0) blocks = std::min(blocks, std::max(1, b.max_groups / per_block));
+    return blocks;
 }
 
 } // namespace fw2v
@@ -928,7 +947,7 @@ template <int LANES, int VEC, int WF, int NC>
 cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, bool fast, bool lifetime,
                           DevCounters* ctr, cudaStream_t st, int* resident) {
     constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;  // RING does not change THREADS
-    const int blocks = (b.n_sentences + per_block - 1) / per_block;
+    const int blocks = k1s_grid(b, per_block);
     if (n_neg + 1 > NC) {
         // Chunks of NC samples; in lifetime order each chunk is its own wavefront,
         // started from the contexts the previous chunk left (exact order).
@@ -967,7 +986,7 @@ template <int LANES, int VEC, int WF, int NC>
 cudaError_t launch_k1s_snap_multi(const ModelView& m, const BatchView& b, int n_neg, bool fast, DevCounters* ctr,
                                   cudaStream_t st, int* resident) {
     constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;
-    const int blocks = (b.n_sentences + per_block - 1) / per_block;
+    const int blocks = k1s_grid(b, per_block);
     return fast ? launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, true, true, false>(blocks, m, b, n_neg, ctr, st, resident)
                 : launch_k1s_inst<LANES, VEC, WF, NC, kMultiChunk, false, true, false>(blocks, m, b, n_neg, ctr, st, resident);
 }

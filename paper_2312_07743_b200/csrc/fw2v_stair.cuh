@@ -48,7 +48,11 @@ struct StairCfg {
     static constexpr int kGroupFloats = (2 * NC + 1) * STRIDE;
     static constexpr int kBlockBytes = (THREADS / LANES) * kGroupFloats * 4;
     static constexpr int kSmemBlocks = (227 * 1024) / (kBlockBytes + 1024);
+#ifdef FW2V_STAIR_REG_BLOCKS  // experiments (tools/variant_lib.sh)
+    static constexpr int kRegBlocks = FW2V_STAIR_REG_BLOCKS;
+#else
     static constexpr int kRegBlocks = VEC < 8 ? 3 : 4;
+#endif
     static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
 };
 
@@ -56,8 +60,8 @@ struct StairCfg {
 // lanes 0..5 and HALF..HALF+5 of the group), N = 5, Hogwild overwrite of the
 // context rows.
 template <int LANES, int VEC, int WF, bool FAST>
-__global__ void __launch_bounds__(StairCfg<LANES, VEC, WF>::THREADS, StairCfg<LANES, VEC, WF>::MINB)
-k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
+__device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchView& b, DevCounters* __restrict__ ctr,
+                                               int sent0) {
     using CF = StairCfg<LANES, VEC, WF>;
     constexpr int NC = CF::NC, NN = NC - 1, NCTX = CF::NCTX, NQ = CF::NQ, OFF = CF::OFF, T = CF::T;
     constexpr int H2 = VEC / 2;
@@ -71,7 +75,7 @@ k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
     const int lane = threadIdx.x & 31;
     const int sub = static_cast<int>(threadIdx.x) & (LANES - 1);
     const int grp = lane / LANES;
-    const int sent = static_cast<int>((blockIdx.x * CF::THREADS + threadIdx.x) / LANES);
+    const int sent = sent0 + static_cast<int>(threadIdx.x / LANES);
     const bool has = sent < b.n_sentences;
     float* sbuf = k1s_sh + (threadIdx.x / LANES) * CF::kGroupFloats + sub * SL::CW;  // + (parity*NC + k)*STRIDE
 
@@ -140,8 +144,10 @@ k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
     };
     // Repeats of a window (ids idw): inside the window (dup), or shared with the
     // previous window (ids idv; lanes HALF.. of the group carry them to the match).
-    auto repeats = [&](int idw, int idv, bool& dup) {
-        const unsigned mm = __match_any_sync(kFull, sub < HALF ? idw : idv);
+    // The match is issued at step T and its votes taken at the end of the
+    // iteration (off the critical path: MATCH has a long latency).
+    auto repeats_issue = [&](int idw, int idv) { return __match_any_sync(kFull, sub < HALF ? idw : idv); };
+    auto repeats = [&](unsigned mm, bool& dup) {
         const unsigned lower = ((1u << HALF) - 1u) << gl;
         const unsigned upper = lower << HALF;
         dup = __any_sync(kFull, sub < HALF && __popc(mm & lower) > 1);
@@ -150,7 +156,8 @@ k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
 
     prefetch(idc, 0);
     bool dup_n = false;
-    bool stale_n = repeats(idc, -1 - lane, dup_n);  // window 0 (no previous window: never stale)
+    bool stale_n = repeats(repeats_issue(idc, -1 - lane), dup_n);  // window 0 (no previous window: never stale)
+    unsigned mm_n = 0;
 
     auto dot = [&](const float2 (&c)[H2], const float2 (&s)[H2]) {
         float2 acc = __fmul2_rn(c[0], s[0]);
@@ -290,7 +297,7 @@ k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
             idn = make_id(qtok[WF + 1], nr_next, nact);
             if (i + 1 < Lmax) prefetch(idn, (i + 1) & 1);
             else cp_async_commit();  // the slide below waits for all but the newest group
-            stale_n = repeats(idn, idc, dup_n);
+            mm_n = repeats_issue(idn, idc);
         };
         if (!dup) {
             // Sample rows enter one step before their first pairing.
@@ -337,6 +344,7 @@ k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
             tact = false;
             tvm = 0;
         }
+        stale_n = repeats(mm_n, dup_n);
         if (wact) {
             s_rw += NC;
             pairs += static_cast<unsigned>(__popc(qv & ~(1u << WF))) * NC;
@@ -392,6 +400,16 @@ k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
             atomicAdd(&ctr->sentences, v6);
         }
     }
+    cp_async_wait_group<0>();  // the staging buffers are the next sentence's
+}
+
+// Blocks stride over the batch's sentences (BatchView::max_groups caps the grid).
+template <int LANES, int VEC, int WF, bool FAST>
+__global__ void __launch_bounds__(StairCfg<LANES, VEC, WF>::THREADS, StairCfg<LANES, VEC, WF>::MINB)
+k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
+    constexpr int PB = StairCfg<LANES, VEC, WF>::THREADS / LANES;
+    for (int s0 = static_cast<int>(blockIdx.x) * PB; s0 < b.n_sentences; s0 += static_cast<int>(gridDim.x) * PB)
+        stair_sentence<LANES, VEC, WF, FAST>(m, b, ctr, s0);
 }
 
 template <int LANES, int VEC, int WF, bool FAST>
@@ -404,8 +422,7 @@ cudaError_t launch_k1s_stair(const ModelView& m, const BatchView& b, DevCounters
         return e;
     constexpr int threads = CF::THREADS;
     if (resident != nullptr) return resident_sentences(kern, bytes, threads, threads / LANES, resident);
-    const int per_block = threads / LANES;
-    const int blocks = (b.n_sentences + per_block - 1) / per_block;
+    const int blocks = k1s_grid(b, threads / LANES);
     if (blocks == 0) return cudaSuccess;
     kern<<<blocks, threads, bytes, st>>>(m, b, ctr);
     return cudaGetLastError();

@@ -23,7 +23,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libfw2v.so")
+LIB_PATH = os.environ.get("FW2V_LIB") or os.path.join(LIB_DIR, "libfw2v.so")  # FW2V_LIB: experiment builds
 DROPIN_PATH = os.path.join(LIB_DIR, "libringvec_fw2v.so")
 
 REUSE_MODES = {"lifetime": 0, "window": 1, "none": 2, "window_snapshot": 3}
@@ -48,7 +48,7 @@ EXPORTED = [
     "fw2v_corpus_view", "fw2v_corpus_free", "fw2v_write_embeddings", "fw2v_save_model",
     "fw2v_nearest_neighbors", "fw2v_eval_analogy", "fw2v_alias_draws", "fw2v_plan_chunks",
     "fw2v_average", "fw2v_nccl_unique_id", "fw2v_comm_init_rank", "fw2v_train_corpus_multi",
-    "fw2v_merge_begin", "fw2v_merge_replicas",
+    "fw2v_merge_begin", "fw2v_merge_replicas", "fw2v_release_cached",
 ]
 
 
