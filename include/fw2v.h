@@ -38,7 +38,7 @@ enum fw2v_status {
     FW2V_ERR_CUDA = 64,        /* CUDA runtime failure (message has the CUDA error string) */
     FW2V_ERR_UNSUPPORTED = 65, /* shape the B200 kernels do not cover (e.g. W_f > 5 on K1) */
     FW2V_ERR_NO_DEVICE = 66,   /* no CUDA device: there is no CPU fallback by design */
-    FW2V_ERR_DIVERGED = 67     /* Hogwild training stayed non-finite after the divergence guard's retries */
+    FW2V_ERR_DIVERGED = 67     /* Hogwild training stayed diverged (non-finite or |x| >= 1e6) after the divergence guard's retries */
 };
 
 enum fw2v_reuse_mode { /* ringvec::ReuseMode (traffic.hpp:15) */
@@ -99,7 +99,8 @@ typedef struct fw2v_config {
                               2 sum: b + sum d_r (every update applied, like Hogwild with the round as
                               staleness) */
     int32_t divergence_guard; /* Hogwild fw2v_train_corpus: 1 = keep the model of the epoch start in HBM
-                                 and check the model is finite after the epoch; if not, restore it,
+                                 and check the model after the epoch (every value finite and below 1e6
+                                 in magnitude: a Hogwild blow-up); if not, restore it,
                                  halve the in-flight budget and train the epoch again (up to 4 times,
                                  then FW2V_ERR_DIVERGED). 0 = off (no snapshot, no check) */
 } fw2v_config;

@@ -6,6 +6,8 @@
 
 #include <cstdint>
 
+#include "fw2v_device.cuh"
+
 namespace fw2v {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -116,6 +118,15 @@ __device__ __forceinline__ void row_load_early(float2 (&v)[H2], const float* p) 
         const float4 t = ldcg_early(p + 2 * i);
         v[i] = make_float2(t.x, t.y);
         v[i + 1] = make_float2(t.z, t.w);
+    }
+}
+
+// One observer-log entry (BatchView::obs_log): called by one lane per sentence
+// before each window, empty windows included (trainer.cpp:246).
+__device__ __forceinline__ void obs_record(const BatchView& b, int sentence, int target) {
+    if (b.obs_log != nullptr) {
+        const unsigned k = atomicAdd(b.obs_count, 1u);
+        b.obs_log[k] = (static_cast<unsigned long long>(b.obs_base + sentence) << 32) | static_cast<unsigned>(target);
     }
 }
 

@@ -22,6 +22,12 @@ struct BatchView {
     const float* alpha;
     int32_t n_sentences;
     int32_t max_groups = 0;  // K1s: at most this many sentences in flight (grid-stride launch); 0 = all
+    // Observer log (test mode, trainer.hpp:82-87): every kernel appends
+    // (sentence in batch) << 32 | target for each window it starts, in the
+    // device's processing order; the host replays it into the observer.
+    unsigned long long* obs_log = nullptr;
+    unsigned int* obs_count = nullptr;
+    int32_t obs_base = 0;  // batch index of sentence 0 of this launch (split launches)
 };
 
 // Embedding matrices in HBM: row w of syn0 (reference `input`, context side)

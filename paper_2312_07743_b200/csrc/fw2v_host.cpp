@@ -651,6 +651,9 @@ struct Slot {
     uint32_t* d_off = nullptr;
     int32_t* d_negs = nullptr;
     float* d_alpha = nullptr;
+    unsigned long long* d_obs = nullptr;  // observer log (test mode), cap_words entries + count
+    unsigned* d_obs_n = nullptr;
+    uint64_t obs_cap = 0;
     cudaEvent_t h2d_done = nullptr;  // host buffers free again (copy stream)
     cudaEvent_t used = nullptr;      // device buffers free again (kernel done, compute stream)
     bool in_flight = false;
@@ -669,7 +672,8 @@ struct Lane {
             BufferPool& pool = BufferPool::get();
             for (void* p : {static_cast<void*>(s.h_ids), static_cast<void*>(s.h_off), static_cast<void*>(s.h_negs),
                             static_cast<void*>(s.h_alpha), static_cast<void*>(s.d_ids), static_cast<void*>(s.d_off),
-                            static_cast<void*>(s.d_negs), static_cast<void*>(s.d_alpha)})
+                            static_cast<void*>(s.d_negs), static_cast<void*>(s.d_alpha), static_cast<void*>(s.d_obs),
+                            static_cast<void*>(s.d_obs_n)})
                 pool.put(p);
             if (s.h2d_done) cudaEventDestroy(s.h2d_done);
             if (s.used) cudaEventDestroy(s.used);
@@ -801,6 +805,7 @@ struct fw2v_ctx {
                 BatchView sub = bv;
                 sub.offsets = bv.offsets + s0;
                 sub.alpha = bv.alpha + s0;
+                sub.obs_base = bv.obs_base + static_cast<int32_t>(s0);
                 sub.n_sentences = static_cast<int32_t>(std::min<int64_t>(cap, bv.n_sentences - s0));
                 cudaError_t e = launch_one(sub, false, ctr, st);
                 if (e != cudaSuccess) return e;
@@ -1381,11 +1386,16 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
                             analytic(sl.h_off[q + 1] - sl.h_off[q], x->wf, n_neg, cfg.reuse_mode, t);
                             for (int z = 0; z < 5; ++z) an[z] += t[z];
                         }
-                        if (sh.observer) {
-                            const uint64_t s0_ = sh.serial.fetch_add(kept);
-                            std::lock_guard<std::mutex> lk(sh.obs_mutex);
-                            for (uint64_t q = 0; q < kept; ++q)
-                                for (uint32_t i = 0; i < sl.h_off[q + 1] - sl.h_off[q]; ++i) sh.observer(sh.observer_user, s0_ + q, i);
+                        // Observer (test mode): serial numbers in batch order; the calls
+                        // are replayed from the kernel's own (sentence, target) log below.
+                        const uint64_t obs_serial0 = sh.observer ? sh.serial.fetch_add(kept) : 0;
+                        if (sh.observer && sl.obs_cap < words) {
+                            BufferPool& pool = BufferPool::get();
+                            pool.put(sl.d_obs);
+                            pool.put(sl.d_obs_n);
+                            sl.d_obs = static_cast<unsigned long long*>(pool.device(8 * words));
+                            sl.d_obs_n = static_cast<unsigned*>(pool.device(sizeof(unsigned)));
+                            sl.obs_cap = words;
                         }
                         // H2D on the lane's copy stream once the kernel that last read
                         // this slot's device buffers is done; the kernel waits for the copy.
@@ -1399,7 +1409,12 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
                         FW2V_CK(cudaStreamWaitEvent(st, sl.h2d_done, 0));
                         sl.in_flight = true;
                         h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
-                        const BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
+                        BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
+                        if (sh.observer) {
+                            FW2V_CK(cudaMemsetAsync(sl.d_obs_n, 0, sizeof(unsigned), st));
+                            bv.obs_log = sl.d_obs;
+                            bv.obs_count = sl.d_obs_n;
+                        }
                         TraceRec rec{};
                         if (trace) {
                             rec = TraceRec{th, w0 - t0, 0.0, 0.0, nullptr, nullptr, words};
@@ -1410,6 +1425,17 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
                         }
                         FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, KS * P));
                         FW2V_CK(cudaEventRecord(sl.used, st));
+                        if (sh.observer) {  // replay the device's window order (trainer.cpp:246)
+                            unsigned n_obs = 0;
+                            std::vector<unsigned long long> log(words);
+                            FW2V_CK(cudaStreamSynchronize(st));
+                            FW2V_CK(cudaMemcpy(&n_obs, sl.d_obs_n, sizeof(unsigned), cudaMemcpyDeviceToHost));
+                            if (n_obs > words) fail(FW2V_ERR_CUDA, "observer log overflow");
+                            FW2V_CK(cudaMemcpy(log.data(), sl.d_obs, 8 * n_obs, cudaMemcpyDeviceToHost));
+                            std::lock_guard<std::mutex> lk(sh.obs_mutex);
+                            for (unsigned z = 0; z < n_obs; ++z)
+                                sh.observer(sh.observer_user, obs_serial0 + (log[z] >> 32), log[z] & 0xffffffffu);
+                        }
                         if (trace) {
                             FW2V_CK(cudaEventRecord(rec.k1, st));
                             rec.t2 = wall_seconds() - t0;
@@ -1578,13 +1604,13 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
                 // vocabulary and learning rate): restore the epoch's start, halve
                 // the in-flight budget and train the epoch again (same batches).
                 if (attempt == kGuardRetries)
-                    fail(FW2V_ERR_DIVERGED, "Hogwild training diverged (non-finite model) at every in-flight budget tried; "
+                    fail(FW2V_ERR_DIVERGED, "Hogwild training diverged (non-finite or |x| >= 1e6 model) at every in-flight budget tried; "
                                             "set max_inflight lower or train with deterministic = 1");
                 guard_restore(x);
                 x->words_trained = words0;
                 guard_halve_inflight(x);
                 ++rep.guard_retries;
-                std::fprintf(stderr, "[fw2v] epoch %d: non-finite model, restored; in-flight budget -> %lld sentences\n",
+                std::fprintf(stderr, "[fw2v] epoch %d: diverged (non-finite or |x| >= 1e6), restored; in-flight budget -> %lld sentences\n",
                              epoch, static_cast<long long>(x->inflight_total));
             }
             const double secs = wall_seconds() - t0;

@@ -97,6 +97,7 @@ k1_lifetime(ModelView m, BatchView b, int n_neg, DevCounters* __restrict__ ctr) 
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
         const bool wact = act && L >= 2;
+        if (sub == 0 && act) obs_record(b, sent, i);
         // Row entering the span for window i+1 (ContextRing::advance, trainer.cpp:55-69).
         const int q = i + 1 + WF;
         const int inc_tok = q < L ? __ldg(ids + q) : -1;
@@ -328,6 +329,7 @@ k2_exact(ModelView m, BatchView b, int n_neg, int wf, int mode, int serial,
             __syncwarp();
             int next_load = 0;
             for (int i = 0; i < L; ++i) {
+                if (lane == 0) obs_record(b, sidx, i);
                 const int hi = min(L - 1, i + wf);  // advance (trainer.cpp:55-69)
                 while (next_load <= hi) {
                     const int slot = next_load % cap;
@@ -423,6 +425,7 @@ k2_exact(ModelView m, BatchView b, int n_neg, int wf, int mode, int serial,
         } else if (mode == kWindow) {
             // train_sentence_window (trainer.cpp:257-290)
             for (int i = 0; i < L; ++i) {
+                if (lane == 0) obs_record(b, sidx, i);
                 const int lo = max(0, i - wf), hh = min(L - 1, i + wf);
                 int n_ctx = 0;
                 for (int j = lo; j <= hh; ++j)
@@ -459,6 +462,7 @@ k2_exact(ModelView m, BatchView b, int n_neg, int wf, int mode, int serial,
         } else {
             // train_sentence_direct (trainer.cpp:292-328)
             for (int i = 0; i < L; ++i) {
+                if (lane == 0) obs_record(b, sidx, i);
                 const int lo = max(0, i - wf), hh = min(L - 1, i + wf);
                 int n_ctx = 0;
                 for (int j = lo; j <= hh; ++j)
@@ -611,14 +615,17 @@ cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t 
     return cudaGetLastError();
 }
 
-// Divergence guard: *flag |= 1 if any of the n floats at p is not finite
-// (one read of the matrix; 16-byte loads, grid sized to the SMs).
+// Divergence guard: *flag |= 1 if any of the n floats at p is not finite or
+// exceeds kDiverged in magnitude (a Hogwild run that blew up: SGNS embeddings
+// stay O(1-10); one read of the matrix, 16-byte loads, grid sized to the SMs).
+constexpr float kDiverged = 1e6f;
 __global__ void k_nonfinite(const float4* __restrict__ p, size_t n4, int* flag) {
     bool bad = false;
     for (size_t x = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; x < n4;
          x += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const float4 v = __ldcg(p + x);
-        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+        // !(|v| < kDiverged) is also true for NaN
+        bad |= !(fabsf(v.x) < kDiverged && fabsf(v.y) < kDiverged && fabsf(v.z) < kDiverged && fabsf(v.w) < kDiverged);
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }

@@ -432,6 +432,7 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
         const bool wact = act && L >= 2;
+        if (sub == 0 && act) obs_record(b, sent, i);
         const int q_in = i + 1 + WF;
         // Token ids run one window ahead of their rows and negatives two; loads
         // issued early are carried raw and masked where consumed. The
@@ -889,6 +890,9 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
         }
     }
     cp_async_wait_group<0>();  // the staging buffers are the next sentence's
+    // Two-warp groups: the next sentence's first exchange must not overwrite a
+    // buffer the other warp is still reading from this sentence's last one.
+    if constexpr (SM::NWG > 1) __syncthreads();
 }
 
 // Blocks stride over the batch's sentences (BatchView::max_groups caps the grid:

@@ -338,6 +338,7 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
         const bool wact = act && L >= 2;
+        if (sub == 0 && act) obs_record(b, sent, i);
         const int q_in = i + 1 + WF;
         const float* cur = sbuf + (i & 1) * NC * STRIDE;
         const float* prv = sbuf + ((i + 1) & 1) * NC * STRIDE;
