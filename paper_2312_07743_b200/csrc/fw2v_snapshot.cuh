@@ -975,8 +975,10 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
             return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
                             : launch_k1s_mode<LANES, VEC, WF, NC, kPartChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);
         // Lifetime order, N = 5, Hogwild overwrite, fast sigmoid: the window staircase.
-        // (W_f <= 3: wider windows spill with both windows' rows live.)
-        if constexpr (NC == 6 && (LANES == 16 || LANES == 32) && WF <= 3 && (VEC == 4 || VEC == 8 || VEC == 10)) {
+        // At W_f = 4-5 both windows' rows spill some registers: still faster at
+        // 4-8 columns per lane (profiles/r02q_stair_wide_windows.txt), not at 10.
+        if constexpr (NC == 6 && (LANES == 16 || LANES == 32) && WF <= 5 && (VEC == 4 || VEC == 8 || VEC == 10) &&
+                      (WF <= 3 || VEC != 10)) {
             if (lifetime && fast && (m.flags & kFlagNoRing) != 0 && (m.flags & kFlagNoStair) == 0)
                 return launch_k1s_stair<LANES, VEC, WF, true>(m, b, ctr, st, resident);
         }

@@ -38,7 +38,11 @@ struct StairCfg {
     static constexpr int NC = 6;                       // samples per window (N = 5)
     static constexpr int NCTX = 2 * WF;
     static constexpr int NQ = 2 * WF + 1;              // ring rows in registers
-    static constexpr int OFF = NC + 1;                 // window-to-window offset in steps
+    static constexpr int STEPS_ = NC + 2 * WF - 1;
+    // Window-to-window offset in steps: >= NC + 1 (the first sample of window i+1
+    // touches a context row after the last sample of window i), and more than half
+    // a window so that only two windows are ever live (W_f = 5: 8).
+    static constexpr int OFF = (NC + 1 > STEPS_ / 2 + 1) ? NC + 1 : STEPS_ / 2 + 1;
     static constexpr int STEPS = NC + NCTX - 1;        // one window's wavefront
     static constexpr int T = STEPS > OFF ? STEPS - OFF : 0;  // tail steps run in the next iteration
     static constexpr int STRIDE = LANES * VEC;
@@ -71,11 +75,6 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     static_assert(VEC % 2 == 0, "8- or 16-byte chunks");
     using SL = Slice<H2, LANES>;
     extern __shared__ __align__(16) float k1s_sh[];
-#ifdef FW2V_STAIR_RS
-    constexpr bool kRS = true;
-#else
-    constexpr bool kRS = false;
-#endif
 
     const int lane = threadIdx.x & 31;
     const int sub = static_cast<int>(threadIdx.x) & (LANES - 1);
@@ -205,131 +204,37 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     bool tact = false;  // the previous window's tail is pending
     unsigned tvm = 0;   // tail validity per ring row (previous window, current indexing)
 
-    // Reduce-scatter plan (kRS): in head step t the step's m dots are reduced by
-    // a transposed butterfly (each level keeps one of a pair of partial sums and
-    // ships the other), so every lane ends with the full sum of ONE dot, whose
-    // sigmoid it evaluates; the m g values then go to every lane by shuffle.
-    // Same additions in the same order as the all-reduce (bitwise equal). The
-    // lane's dot per step is fixed: byte t of desc = ring row | tail << 3 |
-    // label << 4.
-    unsigned desc[(OFF + 3) / 4] = {};
-    if constexpr (kRS) {
-#pragma unroll
-        for (int t = 0; t < OFF; ++t) {
-            int list[NC], iv[NC];
-            int m = 0;
-#pragma unroll
-            for (int k = 0; k < NC; ++k) {
-                const int jh = t - k, jt = t + OFF - k;
-                if ((jh >= 0 && jh < NCTX) || (jt >= 0 && jt < NCTX)) list[m++] = k;
-            }
-#pragma unroll
-            for (int p = 0; p < NC; ++p) iv[p] = p;
-            int n = m;
-#pragma unroll
-            for (int o = LANES / 2; o > 0; o >>= 1) {
-                const bool bit = (sub & o) != 0;
-                const int h = n / 2;
-#pragma unroll
-                for (int p = 0; p < NC / 2; ++p)
-                    if (p < h) iv[p] = bit ? iv[2 * p + 1] : iv[2 * p];
-                if (n & 1) iv[h] = iv[n - 1];
-                n = h + (n & 1);
-            }
-            int k = 0;
-#pragma unroll
-            for (int z = 0; z < NC; ++z)
-                if (z < m && iv[0] == z) k = list[z];
-            const int jh = t - k;
-            const bool head = jh >= 0 && jh < NCTX;
-            const int r = head ? (jh < WF ? jh : jh + 1) : ((t + OFF - k) < WF ? (t + OFF - k) - 1 : (t + OFF - k));
-            const unsigned d = static_cast<unsigned>(r) | (head ? 0u : 8u) | (k == 0 && head ? 16u : 0u);
-            desc[t >> 2] |= d << (8 * (t & 3));
-        }
-    }
-    // The lane that ends with compact dot q of an m-dot step (the butterfly's inverse).
-    auto owner_lane = [](int m, int q) {
-        int lane_ = 0, n = m, p = q;
-#pragma unroll
-        for (int o = LANES / 2; o > 0; o >>= 1) {
-            const int h = n / 2;
-            if (p < 2 * h) {
-                if (p & 1) lane_ |= o;
-                p >>= 1;
-            } else {
-                p = h;
-            }
-            n = h + (n & 1);
-        }
-        return lane_;
-    };
-
     // One step t of iteration i: head pairings (k, t-k) of window i, tail
     // pairings (k, t+OFF-k) of window i-1.
     // (t and HEAD are constants once the step loops below are unrolled.)
     auto step = [&](const int t, const bool HEAD, unsigned hvm, const float* cur, const float* prv, bool wact) {
-        float f[NC];
+        // At W_f >= 4 a sample index can have a head and a tail pairing in one step
+        // (rows Sc[k] and Sp[k]): separate arrays.
+        float fh[NC], ft[NC];
+        auto hd = [&](int k) { return HEAD && t - k >= 0 && t - k < NCTX; };
+        auto tl = [&](int k) { return t + OFF - k >= 0 && t + OFF - k < NCTX; };
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            const int jh = t - k, jt = t + OFF - k;
-            if (HEAD && jh >= 0 && jh < NCTX) f[k] = dot(Q[rh(jh)], Sc[k]);
-            else if (jt >= 0 && jt < NCTX) f[k] = dot(Q[rt(jt)], Sp[k]);
+            if (hd(k)) fh[k] = dot(Q[rh(t - k)], Sc[k]);
+            if (tl(k)) ft[k] = dot(Q[rt(t + OFF - k)], Sp[k]);
         }
-        float gk[NC];  // kRS: g of every dot of the step
-        if (kRS && HEAD) {
-            float v[NC];
-            int m = 0;
+#pragma unroll
+        for (int o = LANES / 2; o > 0; o >>= 1)
 #pragma unroll
             for (int k = 0; k < NC; ++k) {
-                const int jh = t - k, jt = t + OFF - k;
-                if ((jh >= 0 && jh < NCTX) || (jt >= 0 && jt < NCTX)) v[m++] = f[k];
+                if (hd(k)) fh[k] += __shfl_xor_sync(kFull, fh[k], o);
+                if (tl(k)) ft[k] += __shfl_xor_sync(kFull, ft[k], o);
             }
-            int n = m;
-#pragma unroll
-            for (int o = LANES / 2; o > 0; o >>= 1) {
-                const bool bit = (sub & o) != 0;
-                const int h = n / 2;
-#pragma unroll
-                for (int p = 0; p < NC / 2; ++p)
-                    if (p < h) {
-                        const float a = v[2 * p], b2 = v[2 * p + 1];
-                        v[p] = (bit ? b2 : a) + __shfl_xor_sync(kFull, bit ? a : b2, o);
-                    }
-                if (n & 1) v[h] = v[n - 1] + __shfl_xor_sync(kFull, v[n - 1], o);
-                n = h + (n & 1);
-            }
-            const unsigned d = (desc[t >> 2] >> (8 * (t & 3))) & 31u;
-            const unsigned vm = (d & 8u) ? tvm : hvm;
-            const float g = coeff(v[0], ((vm >> (d & 7u)) & 1u) ? nha : 0.0f, (d & 16u) != 0u);
-            int q = 0;
-#pragma unroll
-            for (int k = 0; k < NC; ++k) {
-                const int jh = t - k, jt = t + OFF - k;
-                if ((jh >= 0 && jh < NCTX) || (jt >= 0 && jt < NCTX)) gk[k] = __shfl_sync(kFull, g, gl + owner_lane(m, q++));
-            }
-        } else {
-#pragma unroll
-            for (int o = LANES / 2; o > 0; o >>= 1)
-#pragma unroll
-                for (int k = 0; k < NC; ++k) {
-                    const int jh = t - k, jt = t + OFF - k;
-                    if ((HEAD && jh >= 0 && jh < NCTX) || (jt >= 0 && jt < NCTX)) f[k] += __shfl_xor_sync(kFull, f[k], o);
-                }
-#pragma unroll
-            for (int k = 0; k < NC; ++k) {
-                const int jh = t - k, jt = t + OFF - k;
-                if (HEAD && jh >= 0 && jh < NCTX) gk[k] = coeff(f[k], ((hvm >> rh(jh)) & 1u) ? nha : 0.0f, k == 0);
-                else if (jt >= 0 && jt < NCTX) gk[k] = coeff(f[k], ((tvm >> rt(jt)) & 1u) ? nha : 0.0f, k == 0);
-            }
-        }
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            const int jh = t - k, jt = t + OFF - k;
-            if (HEAD && jh >= 0 && jh < NCTX) {
-                update(Q[rh(jh)], Sc[k], gk[k]);
+            if (hd(k)) {
+                const int jh = t - k;
+                update(Q[rh(jh)], Sc[k], coeff(fh[k], ((hvm >> rh(jh)) & 1u) ? nha : 0.0f, k == 0));
                 if (jh == NCTX - 1) writeback(Sc[k], cur + k * STRIDE, __shfl_sync(kFull, idc, gl + k), wact);
-            } else if (jt >= 0 && jt < NCTX) {
-                update(Q[rt(jt)], Sp[k], gk[k]);
+            }
+            if (tl(k)) {
+                const int jt = t + OFF - k;
+                update(Q[rt(jt)], Sp[k], coeff(ft[k], ((tvm >> rt(jt)) & 1u) ? nha : 0.0f, k == 0));
                 if (jt == NCTX - 1) writeback(Sp[k], prv + k * STRIDE, __shfl_sync(kFull, idp, gl + k), tact);
             }
         }

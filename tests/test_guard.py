@@ -33,26 +33,33 @@ def test_guard_unreachable_rate_fails_loudly(text8):
 
 
 def test_guard_restores_and_retrains():
-    """The DESIGN.md §5 blow-up: the text8 shape without hot-row replicas and
-    every sentence of a batch in flight at the reference rate (0.025) diverges
-    within 5 epochs (3,000+ sentences in flight on the same hot rows). With the
-    guard the diverged epoch is restored and retrained with fewer sentences in
-    flight, and the run ends with a sane model."""
+    """A Hogwild blow-up: the text8 shape without hot-row replicas,
+    every sentence of a batch in flight (3,000+ on the same hot rows), 5 epochs,
+    at the first of 0.025 / 0.05 / 0.1 / 0.2 that blows up. With the guard the
+    diverged epoch is restored and retrained with fewer sentences in flight, and
+    the run ends with a sane model."""
     text8 = fw.synth_zipf(**fw.TEXT8_SHAPE)
     cfg = dict(epochs=5, workers=64, streams=16)
 
     def sane(m):
         return np.isfinite(m).all() and np.abs(m).max() < 1e6
 
-    with fw.Trainer(_cfg(divergence_guard=0, **cfg), text8.counts) as t:
-        t.train_corpus(text8)
+    for alpha0 in (0.025, 0.05, 0.1, 0.2):  # the first rate that blows up uncapped
+        with fw.Trainer(_cfg(divergence_guard=0, alpha0=alpha0, **cfg), text8.counts) as t:
+            t.train_corpus(text8)
+            gi, go = t.get_model()
+        if not (sane(gi) and sane(go)):
+            break
+    else:
+        pytest.skip("no tested rate blew up uncapped")
+    with fw.Trainer(_cfg(alpha0=alpha0, **cfg), text8.counts) as t:
+        try:
+            rep = t.train_corpus(text8)
+        except fw.Fw2vError as e:
+            assert e.code == 67
+            pytest.skip(f"alpha0={alpha0} diverges at every budget tried")
         gi, go = t.get_model()
-    if sane(gi) and sane(go):
-        pytest.skip("this run did not blow up uncapped")
-    with fw.Trainer(_cfg(**cfg), text8.counts) as t:
-        rep = t.train_corpus(text8)
-        gi, go = t.get_model()
-    print(f"guard retries {rep.guard_retries}, max |x| {max(np.abs(gi).max(), np.abs(go).max()):.3g}")
+    print(f"alpha0={alpha0}: guard retries {rep.guard_retries}, max |x| {max(np.abs(gi).max(), np.abs(go).max()):.3g}")
     assert rep.guard_retries >= 1
     assert sane(gi) and sane(go)
 

@@ -54,7 +54,7 @@ def _disjoint_launch(rng, n_sent, band, lens, n_neg, types_per_band):
 
 
 @pytest.mark.parametrize("dim", [64, 128, 256, 300])
-@pytest.mark.parametrize("window", [2, 4, 5, 6])
+@pytest.mark.parametrize("window", [2, 4, 5, 6, 8, 10])
 @pytest.mark.parametrize("types_per_band", [7, 40, 500], ids=["repeats", "some", "rare"])
 def test_stair_equals_wavefront_bitwise(dim, window, types_per_band):
     n_neg = 5
