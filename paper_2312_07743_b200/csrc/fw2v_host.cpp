@@ -935,12 +935,14 @@ uint64_t expected_epoch_words(const fw2v_ctx& x) {  // trainer.cpp:378-386
 // probability p_w ~ count^power; with M sentences in flight, a drawn row is
 // being updated by ~M (N+1) sum_w p_w^2 = M (N+1) / V_eff sentences at the
 // same time, and their summed deltas act as one step of that many times alpha.
-// The cap keeps M (N+1) alpha / V_eff <= 8 x 0.025. Measured on the text8
-// shape (d=128, 5 epochs): 2,960 sentences in flight diverge (loss 3e18) with
-// V_eff = 1,472, 1,776 train to within 0.5% of the reference. Hot-row
+// The cap keeps M (N+1) alpha / V_eff <= 20 x 0.025. Measured on the text8
+// shape (d=128, 5 epochs, no replicas, V_eff = 1,472; profiles/r02_budget_probe.txt):
+// every sentence of a batch in flight (3,552 resident) trains to within 0.5% of
+// the reference at alpha 0.025 and blows up at 0.1 (the divergence guard then
+// halves the budget); round 1 used 8 x 0.025, tuned on an earlier kernel. Hot-row
 // replicas (fw2v_config.hot_rows) split the top rows' traffic R ways, which
 // lifts V_eff to ~9,700 there; the reference's 60-word pipeline test
-// (V_eff = 60, alpha 0.05) is held to 40 sentences.
+// (V_eff = 60, alpha 0.05) is held to 100 sentences.
 int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power, int n_neg, float alpha0, int hot_k,
                       int hot_r, int dim) {
     double z = 0.0, z2 = 0.0;
@@ -953,7 +955,7 @@ int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power, 
     // Wide rows tolerate less staleness (measured on the planted corpus: d=512 at
     // 888 sentences in flight +2.3% loss, at 512 +0.7%; d=128 fine at 3,552).
     const double wide = dim > 128 ? (128.0 / dim) * (128.0 / dim) : 1.0;
-    const double m = 8.0 * 0.025 * v_eff / ((n_neg + 1) * static_cast<double>(alpha0)) * wide;
+    const double m = 20.0 * 0.025 * v_eff / ((n_neg + 1) * static_cast<double>(alpha0)) * wide;
     return std::max<int64_t>(32, static_cast<int64_t>(std::ceil(m)));
 }
 
