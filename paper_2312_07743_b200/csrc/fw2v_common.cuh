@@ -130,6 +130,16 @@ __device__ __forceinline__ void obs_record(const BatchView& b, int sentence, int
     }
 }
 
+// All L windows of a sentence at once (the Hogwild kernels log when a sentence
+// starts, outside their window loop; per sentence the targets are in order).
+__device__ __forceinline__ void obs_record_sentence(const BatchView& b, int sentence, int L) {
+    if (b.obs_log != nullptr && L > 0) {
+        const unsigned k0 = atomicAdd(b.obs_count, static_cast<unsigned>(L));
+        const unsigned long long s = static_cast<unsigned long long>(b.obs_base + sentence) << 32;
+        for (int i = 0; i < L; ++i) b.obs_log[k0 + i] = s | static_cast<unsigned>(i);
+    }
+}
+
 template <int H2>
 __device__ __forceinline__ void vzero2(float2 (&v)[H2]) {
 #pragma unroll

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -660,6 +661,18 @@ struct Slot {
 };
 
 struct Lane {
+    // A sub-batch assembled and shipped (H2D issued) at the end of one pass for
+    // the next (run_pass cross-epoch prefetch): its slot, size and the span
+    // iteration state to resume from, and its share of the pass statistics.
+    struct Stash {
+        bool ready = false;
+        uint64_t pass = 0;
+        int slot = 0;
+        uint64_t kept = 0, words = 0, p = 0, cursor = 0, end = 0, k = 0, left = 0, h2d = 0;
+        Rng rng{};
+        double cpu = 0.0;
+        uint64_t an[5] = {};
+    } stash;
     cudaStream_t stream = nullptr;  // kernels of slot 0
     cudaStream_t stream2 = nullptr; // kernels of slot 1 (Hogwild: a lane's sub-batches overlap)
     cudaStream_t copy = nullptr;    // H2D of the next sub-batch, overlapping the current kernel
@@ -680,6 +693,7 @@ struct Lane {
             s = Slot{};
         }
         cap_words = cap_sent = 0;
+        stash.ready = false;
     }
 };
 
@@ -718,6 +732,7 @@ struct fw2v_ctx {
     // of the current epoch, [syn0 | syn1], and a device flag word.
     float* guard_snap = nullptr;
     int* guard_flag = nullptr;
+    uint64_t pass_seq = 0;  // run_pass calls so far
     size_t model_floats() const { return static_cast<size_t>(vocab) * static_cast<size_t>(stride); }
 
     int32_t k1_flags = 0;
@@ -954,7 +969,9 @@ int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power, 
     const double v_eff = z2 > 0.0 ? z * z / z2 : 1.0;
     // Wide rows tolerate less staleness (measured on the planted corpus: d=512 at
     // 888 sentences in flight +2.3% loss, at 512 +0.7%; d=128 fine at 3,552).
-    const double wide = dim > 128 ? (128.0 / dim) * (128.0 / dim) : 1.0;
+    // Wide rows keep round 1's measured budget (8 x 0.025 scaled by (128/d)^2):
+    // at d=512 the planted corpus is +2.3% at 20 x 0.025 (tests/test_quality.py).
+    const double wide = dim > 128 ? 0.4 * (128.0 / dim) * (128.0 / dim) : 1.0;
     const double m = 20.0 * 0.025 * v_eff / ((n_neg + 1) * static_cast<double>(alpha0)) * wide;
     return std::max<int64_t>(32, static_cast<int64_t>(std::ceil(m)));
 }
@@ -1242,6 +1259,8 @@ struct RunShared {
     uint64_t origin = 0, scale = 1;
     uint64_t position(uint64_t w) const { return origin + (w - origin) * scale; }
     std::atomic<uint64_t> serial{0};
+    // Whether the last pass already started the next one's reservations.
+    std::atomic<bool> prefetched{false};
     std::mutex obs_mutex;
     fw2v_observer_fn observer = nullptr;
     void* observer_user = nullptr;
@@ -1269,7 +1288,7 @@ void add_counters(fw2v_counters& a, const fw2v_counters& b) {
 // launch on the lane's kernel streams. Hogwild hot-row replicas are broadcast
 // before and averaged after the pass. Returns after every kernel finished.
 void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan>& spans, int epoch, RunShared& sh,
-              PassOut* out) {
+              PassOut* out, const std::vector<ChunkSpan>* next_spans = nullptr) {
     FW2V_CK(cudaSetDevice(x->cfg.device));
     const fw2v_config& cfg = x->cfg;
     const int NS = static_cast<int>(spans.size());
@@ -1283,6 +1302,7 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
         chunk = std::max(chunk, c.end - c.begin);
     }
     x->ensure_lanes(P, cap_w, cap_s);
+    const uint64_t pass = ++x->pass_seq;  // matches a lane's stash to the pass it was made for
     // Sub-batches of ~256-511 sentences (equal parts of a chunk; enough to keep
     // the device full across the streams), never above S.
     static const uint64_t sub_target = [] {
@@ -1341,7 +1361,18 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
     std::atomic<uint64_t> batch_words{0}, batch_nanos{0}, h2d{0};
     const double t0 = wall_seconds();
     std::vector<std::thread> threads;
-    std::atomic<int> next_span{0};
+    // Span claiming: thread th takes span th first (a stashed first sub-batch of
+    // this pass, see below, was assembled from it), then whole spans dynamically.
+    std::atomic<int> next_span{std::min(P, NS)};
+    // Cross-epoch prefetch (Hogwild fw2v_train_corpus): once every thread has
+    // assembled this pass, each assembles and ships (H2D) the first sub-batch of
+    // its first span of the NEXT pass into a free slot, so that pass's kernels
+    // start as soon as this pass's end work (replica average, divergence check)
+    // is done instead of after a host assembly.
+    const bool prefetch = next_spans != nullptr && !x->deterministic && sh.observer == nullptr;
+    int assembled = 0;  // threads done with this pass's spans (under asm_mu)
+    std::mutex asm_mu;
+    std::condition_variable asm_cv;
     for (int th = 0; th < P; ++th) {
         threads.emplace_back([&, th] {
             try {
@@ -1351,99 +1382,189 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
                 uint64_t wsum = 0;
                 uint64_t* an = &an_acc[static_cast<size_t>(th) * 5];
                 int which = 0;
-                for (int si = next_span.fetch_add(1); si < NS; si = next_span.fetch_add(1)) {
-                    const ChunkSpan& cs_ = spans[static_cast<size_t>(si)];
-                    const uint64_t end = cs_.end;
-                    uint64_t cursor = cs_.begin;
-                    // Batch k (reference stream derive(seed, epoch, p, k), S kept
-                    // sentences) is shipped in sub-batches of `sub` sentences drawn
-                    // from the same stream in the same order, so the kernels of one
-                    // sub-batch overlap the host assembly of the next.
-                    Rng rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), cs_.p, 0);
-                    uint64_t k = 0, left = cfg.batch_sentences;
-                    while (cursor < end) {
-                        if (left == 0) {
-                            ++k;
-                            left = cfg.batch_sentences;
-                            rng = Rng::derive(cfg.seed, static_cast<uint64_t>(epoch), cs_.p, k);
+                // Iteration state of one span: batch k (reference stream derive(seed,
+                // epoch, p, k), S kept sentences) is shipped in sub-batches drawn from
+                // the same stream in the same order, so the kernels of one sub-batch
+                // overlap the host assembly of the next.
+                struct SpanIt {
+                    uint64_t p = 0, cursor = 0, end = 0, k = 0, left = 0;
+                    Rng rng;
+                };
+                auto open_span = [&](const ChunkSpan& cs_, int ep) {
+                    SpanIt it;
+                    it.p = cs_.p;
+                    it.cursor = cs_.begin;
+                    it.end = cs_.end;
+                    it.left = cfg.batch_sentences;
+                    it.rng = Rng::derive(cfg.seed, static_cast<uint64_t>(ep), cs_.p, 0);
+                    return it;
+                };
+                // Assembles the next sub-batch of `it` into slot `which` and issues its
+                // H2D; returns kept sentences (0: nothing kept, slot untouched).
+                auto assemble_ship = [&](SpanIt& it, int ep, bool first, uint64_t* words_out, uint64_t* obs0,
+                                         double* w0_out) -> uint64_t {
+                    if (it.left == 0) {
+                        ++it.k;
+                        it.left = cfg.batch_sentences;
+                        it.rng = Rng::derive(cfg.seed, static_cast<uint64_t>(ep), it.p, it.k);
+                    }
+                    Slot& sl = ln.slot[which];
+                    if (sl.in_flight) FW2V_CK(cudaEventSynchronize(sl.h2d_done));
+                    const double c0 = thread_cpu_seconds();
+                    *w0_out = trace ? wall_seconds() : 0.0;
+                    uint64_t words = 0;
+                    const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
+                    // A short first sub-batch per thread gets the device busy early.
+                    const uint64_t want = std::min(it.left, first && first_sub > 0 ? std::min<uint64_t>(sub, first_sub) : sub);
+                    const uint64_t kept = assemble(corpus, it.cursor, it.end, want, sp, it.rng, bo, &words);
+                    it.left -= kept;
+                    // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
+                    const uint64_t base = sh.reserved.fetch_add(words);
+                    for (uint64_t q = 0; q < kept; ++q) sl.h_alpha[q] = lr_at(sh.position(base + sl.h_off[q]), sh.schedule_total, cfg.alpha0);
+                    cpu += thread_cpu_seconds() - c0;
+                    *words_out = words;
+                    if (kept == 0) return 0;
+                    wsum += words;
+                    for (uint64_t q = 0; q < kept; ++q) {
+                        uint64_t t[5];
+                        analytic(sl.h_off[q + 1] - sl.h_off[q], x->wf, n_neg, cfg.reuse_mode, t);
+                        for (int z = 0; z < 5; ++z) an[z] += t[z];
+                    }
+                    // Observer (test mode): serial numbers in batch order; the calls
+                    // are replayed from the kernel's own (sentence, target) log below.
+                    *obs0 = sh.observer ? sh.serial.fetch_add(kept) : 0;
+                    if (sh.observer && sl.obs_cap < words) {
+                        BufferPool& pool = BufferPool::get();
+                        pool.put(sl.d_obs);
+                        pool.put(sl.d_obs_n);
+                        sl.d_obs = static_cast<unsigned long long*>(pool.device(8 * words));
+                        sl.d_obs_n = static_cast<unsigned*>(pool.device(sizeof(unsigned)));
+                        sl.obs_cap = words;
+                    }
+                    // H2D on the lane's copy stream once the kernel that last read
+                    // this slot's device buffers is done; the kernel waits for the copy.
+                    const cudaStream_t cs = ln.copy;
+                    if (sl.in_flight) FW2V_CK(cudaStreamWaitEvent(cs, sl.used, 0));
+                    FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, cs));
+                    if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, cs));
+                    FW2V_CK(cudaMemcpyAsync(sl.d_off, sl.h_off, 4 * (kept + 1), cudaMemcpyHostToDevice, cs));
+                    FW2V_CK(cudaMemcpyAsync(sl.d_alpha, sl.h_alpha, 4 * kept, cudaMemcpyHostToDevice, cs));
+                    FW2V_CK(cudaEventRecord(sl.h2d_done, cs));
+                    sl.in_flight = true;
+                    h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
+                    return kept;
+                };
+                // Launches the sub-batch shipped into slot `which`, then flips the slot.
+                auto launch_slot = [&](uint64_t kept, uint64_t words, uint64_t obs_serial0, double w0) {
+                    Slot& sl = ln.slot[which];
+                    const cudaStream_t st = which == 1 && KS > 1 ? ln.stream2 : ln.stream;
+                    FW2V_CK(cudaStreamWaitEvent(st, sl.h2d_done, 0));
+                    BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
+                    if (sh.observer) {
+                        FW2V_CK(cudaMemsetAsync(sl.d_obs_n, 0, sizeof(unsigned), st));
+                        bv.obs_log = sl.d_obs;
+                        bv.obs_count = sl.d_obs_n;
+                    }
+                    TraceRec rec{};
+                    if (trace) {
+                        rec = TraceRec{th, w0 - t0, 0.0, 0.0, nullptr, nullptr, words};
+                        rec.t1 = wall_seconds() - t0;
+                        FW2V_CK(cudaEventCreate(&rec.k0));
+                        FW2V_CK(cudaEventCreate(&rec.k1));
+                        FW2V_CK(cudaEventRecord(rec.k0, st));
+                    }
+                    FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, KS * P));
+                    FW2V_CK(cudaEventRecord(sl.used, st));
+                    if (sh.observer) {  // replay the device's window order (trainer.cpp:246)
+                        unsigned n_obs = 0;
+                        std::vector<unsigned long long> log(words);
+                        FW2V_CK(cudaStreamSynchronize(st));
+                        FW2V_CK(cudaMemcpy(&n_obs, sl.d_obs_n, sizeof(unsigned), cudaMemcpyDeviceToHost));
+                        if (n_obs > words) fail(FW2V_ERR_CUDA, "observer log overflow");
+                        FW2V_CK(cudaMemcpy(log.data(), sl.d_obs, 8 * n_obs, cudaMemcpyDeviceToHost));
+                        std::lock_guard<std::mutex> lk(sh.obs_mutex);
+                        for (unsigned z = 0; z < n_obs; ++z)
+                            sh.observer(sh.observer_user, obs_serial0 + (log[z] >> 32), log[z] & 0xffffffffu);
+                    }
+                    if (trace) {
+                        FW2V_CK(cudaEventRecord(rec.k1, st));
+                        rec.t2 = wall_seconds() - t0;
+                        tr[static_cast<size_t>(th)].push_back(rec);
+                    }
+                    which ^= 1;
+                };
+                auto run_span = [&](SpanIt it, bool first) {
+                    while (it.cursor < it.end) {
+                        uint64_t words = 0, obs0 = 0;
+                        double w0 = 0.0;
+                        const uint64_t kept = assemble_ship(it, epoch, first && wsum == 0, &words, &obs0, &w0);
+                        if (kept > 0) launch_slot(kept, words, obs0, w0);
+                    }
+                };
+                // This pass's first sub-batch may have been shipped by the previous pass.
+                Lane::Stash& stash = ln.stash;
+                if (stash.ready && stash.pass == pass) {
+                    stash.ready = false;
+                    which = stash.slot;
+                    cpu += stash.cpu;
+                    wsum += stash.words;
+                    for (int z = 0; z < 5; ++z) an[z] += stash.an[z];
+                    h2d.fetch_add(stash.h2d);
+                    launch_slot(stash.kept, stash.words, 0, t0);
+                    SpanIt it;
+                    it.p = stash.p;
+                    it.cursor = stash.cursor;
+                    it.end = stash.end;
+                    it.k = stash.k;
+                    it.left = stash.left;
+                    it.rng = stash.rng;
+                    run_span(it, false);
+                } else if (th < NS) {
+                    run_span(open_span(spans[static_cast<size_t>(th)], epoch), true);
+                }
+                for (int si = next_span.fetch_add(1); si < NS; si = next_span.fetch_add(1))
+                    run_span(open_span(spans[static_cast<size_t>(si)], epoch), true);
+                {
+                    std::lock_guard<std::mutex> lk(asm_mu);
+                    if (++assembled == P) asm_cv.notify_all();
+                }
+                if (prefetch && th < static_cast<int>(next_spans->size())) {
+                    // Every thread's reservations of this pass precede the next pass's.
+                    {
+                        std::unique_lock<std::mutex> lk(asm_mu);
+                        asm_cv.wait(lk, [&] { return assembled == P; });
+                    }
+                    SpanIt it = open_span((*next_spans)[static_cast<size_t>(th)], epoch + 1);
+                    const double cpu0 = cpu;
+                    const uint64_t ws0 = wsum;
+                    uint64_t an0[5];
+                    for (int z = 0; z < 5; ++z) an0[z] = an[z];
+                    uint64_t words = 0, obs0 = 0, kept = 0;
+                    double w0 = 0.0;
+                    while (kept == 0 && it.cursor < it.end) kept = assemble_ship(it, epoch + 1, true, &words, &obs0, &w0);
+                    if (kept > 0) {
+                        // Attributed to the next pass (words, CPU, analytic counters, H2D).
+                        stash.ready = true;
+                        stash.pass = pass + 1;
+                        stash.slot = which;
+                        stash.kept = kept;
+                        stash.words = words;
+                        stash.p = it.p;
+                        stash.cursor = it.cursor;
+                        stash.end = it.end;
+                        stash.k = it.k;
+                        stash.left = it.left;
+                        stash.rng = it.rng;
+                        stash.cpu = cpu - cpu0;
+                        cpu = cpu0;
+                        wsum = ws0;
+                        for (int z = 0; z < 5; ++z) {
+                            stash.an[z] = an[z] - an0[z];
+                            an[z] = an0[z];
                         }
-                        Slot& sl = ln.slot[which];
-                        if (sl.in_flight) FW2V_CK(cudaEventSynchronize(sl.h2d_done));
-                        const double c0 = thread_cpu_seconds();
-                        const double w0 = trace ? wall_seconds() : 0.0;
-                        uint64_t words = 0;
-                        const BatchOut bo{sl.h_ids, sl.h_off, sl.h_negs, ln.cap_words, ln.cap_sent};
-                        // A short first sub-batch per thread gets the device busy early.
-                        const uint64_t want = std::min(left, which == 0 && wsum == 0 && first_sub > 0 ? std::min<uint64_t>(sub, first_sub) : sub);
-                        const uint64_t kept = assemble(corpus, cursor, end, want, sp, rng, bo, &words);
-                        left -= kept;
-                        // Learning rate per sentence from the global schedule (trainer.cpp:479-481).
-                        const uint64_t base = sh.reserved.fetch_add(words);
-                        for (uint64_t q = 0; q < kept; ++q) sl.h_alpha[q] = lr_at(sh.position(base + sl.h_off[q]), sh.schedule_total, cfg.alpha0);
-                        cpu += thread_cpu_seconds() - c0;
-                        wsum += words;
-                        if (kept == 0) continue;
-                        for (uint64_t q = 0; q < kept; ++q) {
-                            uint64_t t[5];
-                            analytic(sl.h_off[q + 1] - sl.h_off[q], x->wf, n_neg, cfg.reuse_mode, t);
-                            for (int z = 0; z < 5; ++z) an[z] += t[z];
-                        }
-                        // Observer (test mode): serial numbers in batch order; the calls
-                        // are replayed from the kernel's own (sentence, target) log below.
-                        const uint64_t obs_serial0 = sh.observer ? sh.serial.fetch_add(kept) : 0;
-                        if (sh.observer && sl.obs_cap < words) {
-                            BufferPool& pool = BufferPool::get();
-                            pool.put(sl.d_obs);
-                            pool.put(sl.d_obs_n);
-                            sl.d_obs = static_cast<unsigned long long*>(pool.device(8 * words));
-                            sl.d_obs_n = static_cast<unsigned*>(pool.device(sizeof(unsigned)));
-                            sl.obs_cap = words;
-                        }
-                        // H2D on the lane's copy stream once the kernel that last read
-                        // this slot's device buffers is done; the kernel waits for the copy.
-                        cudaStream_t st = which == 1 && KS > 1 ? ln.stream2 : ln.stream, cs = ln.copy;
-                        if (sl.in_flight) FW2V_CK(cudaStreamWaitEvent(cs, sl.used, 0));
-                        FW2V_CK(cudaMemcpyAsync(sl.d_ids, sl.h_ids, 4 * words, cudaMemcpyHostToDevice, cs));
-                        if (n_neg) FW2V_CK(cudaMemcpyAsync(sl.d_negs, sl.h_negs, 4 * words * n_neg, cudaMemcpyHostToDevice, cs));
-                        FW2V_CK(cudaMemcpyAsync(sl.d_off, sl.h_off, 4 * (kept + 1), cudaMemcpyHostToDevice, cs));
-                        FW2V_CK(cudaMemcpyAsync(sl.d_alpha, sl.h_alpha, 4 * kept, cudaMemcpyHostToDevice, cs));
-                        FW2V_CK(cudaEventRecord(sl.h2d_done, cs));
-                        FW2V_CK(cudaStreamWaitEvent(st, sl.h2d_done, 0));
-                        sl.in_flight = true;
-                        h2d.fetch_add(4 * (words * (1 + n_neg) + 2 * kept + 1));
-                        BatchView bv{sl.d_ids, sl.d_off, sl.d_negs, sl.d_alpha, static_cast<int32_t>(kept)};
-                        if (sh.observer) {
-                            FW2V_CK(cudaMemsetAsync(sl.d_obs_n, 0, sizeof(unsigned), st));
-                            bv.obs_log = sl.d_obs;
-                            bv.obs_count = sl.d_obs_n;
-                        }
-                        TraceRec rec{};
-                        if (trace) {
-                            rec = TraceRec{th, w0 - t0, 0.0, 0.0, nullptr, nullptr, words};
-                            rec.t1 = wall_seconds() - t0;
-                            FW2V_CK(cudaEventCreate(&rec.k0));
-                            FW2V_CK(cudaEventCreate(&rec.k1));
-                            FW2V_CK(cudaEventRecord(rec.k0, st));
-                        }
-                        FW2V_CK(x->launch(bv, x->deterministic, ln.d_ctr, st, KS * P));
-                        FW2V_CK(cudaEventRecord(sl.used, st));
-                        if (sh.observer) {  // replay the device's window order (trainer.cpp:246)
-                            unsigned n_obs = 0;
-                            std::vector<unsigned long long> log(words);
-                            FW2V_CK(cudaStreamSynchronize(st));
-                            FW2V_CK(cudaMemcpy(&n_obs, sl.d_obs_n, sizeof(unsigned), cudaMemcpyDeviceToHost));
-                            if (n_obs > words) fail(FW2V_ERR_CUDA, "observer log overflow");
-                            FW2V_CK(cudaMemcpy(log.data(), sl.d_obs, 8 * n_obs, cudaMemcpyDeviceToHost));
-                            std::lock_guard<std::mutex> lk(sh.obs_mutex);
-                            for (unsigned z = 0; z < n_obs; ++z)
-                                sh.observer(sh.observer_user, obs_serial0 + (log[z] >> 32), log[z] & 0xffffffffu);
-                        }
-                        if (trace) {
-                            FW2V_CK(cudaEventRecord(rec.k1, st));
-                            rec.t2 = wall_seconds() - t0;
-                            tr[static_cast<size_t>(th)].push_back(rec);
-                        }
-                        which ^= 1;
+                        stash.h2d = 4 * (words * (1 + n_neg) + 2 * kept + 1);
+                        h2d.fetch_sub(stash.h2d);
+                        sh.prefetched.store(true);
                     }
                 }
                 batch_words.fetch_add(wsum);
@@ -1598,10 +1719,14 @@ int fw2v_train_corpus(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_sentences
             for (int attempt = 0;; ++attempt) {
                 const uint64_t words0 = x->words_trained;
                 if (guard) guard_save(x);
-                sh.reserved.store(x->words_trained);
+                // (The previous pass may already have started this one: its first
+                // sub-batches reserved their words.)
+                if (!sh.prefetched.exchange(false)) sh.reserved.store(x->words_trained);
                 o = PassOut{};
-                run_pass(x, corpus, spans, epoch, sh, &o);
+                run_pass(x, corpus, spans, epoch, sh, &o, epoch + 1 < cfg.epochs ? &spans : nullptr);
                 if (!guard || guard_finite(x)) break;
+                for (Lane& ln : x->lanes) ln.stash.ready = false;  // made for the next epoch
+                sh.prefetched.store(false);
                 // Hogwild diverged (too many sentences in flight for this
                 // vocabulary and learning rate): restore the epoch's start, halve
                 // the in-flight budget and train the epoch again (same batches).

@@ -329,6 +329,7 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
         alpha = __ldg(b.alpha + sent);
     }
     const int L = static_cast<int>(len);
+    if (sub == 0) obs_record_sentence(b, sent, L);  // observer (test mode)
     const int Lmax = static_cast<int>(__reduce_max_sync(kFull, len));
     if (Lmax == 0) return;
 
@@ -432,7 +433,6 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
         const bool wact = act && L >= 2;
-        if (sub == 0 && act) obs_record(b, sent, i);
         const int q_in = i + 1 + WF;
         // Token ids run one window ahead of their rows and negatives two; loads
         // issued early are carried raw and masked where consumed. The

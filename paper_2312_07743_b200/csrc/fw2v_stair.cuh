@@ -91,6 +91,7 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
         alpha = __ldg(b.alpha + sent);
     }
     const int L = static_cast<int>(len);
+    if (sub == 0) obs_record_sentence(b, sent, L);  // observer (test mode)
     const int Lmax = static_cast<int>(__reduce_max_sync(kFull, len));
     if (Lmax == 0) return;
     const int32_t* __restrict__ ids = b.ids + beg;
@@ -208,22 +209,28 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     // pairings (k, t+OFF-k) of window i-1.
     // (t and HEAD are constants once the step loops below are unrolled.)
     auto step = [&](const int t, const bool HEAD, unsigned hvm, const float* cur, const float* prv, bool wact) {
-        // At W_f >= 4 a sample index can have a head and a tail pairing in one step
-        // (rows Sc[k] and Sp[k]): separate arrays.
-        float fh[NC], ft[NC];
         auto hd = [&](int k) { return HEAD && t - k >= 0 && t - k < NCTX; };
         auto tl = [&](int k) { return t + OFF - k >= 0 && t + OFF - k < NCTX; };
+        // Up to W_f = 3 a sample index has at most one pairing per step (head rows
+        // k <= t, tail rows k >= t + 2): one dot array. At W_f >= 4 it can have
+        // both (rows Sc[k] and Sp[k]): a second array for the tail.
+        constexpr bool kBoth = NCTX > NC + 1;
+        float fh[NC], ft[kBoth ? NC : 1];
+        auto tf = [&](int k) -> float& {
+            if constexpr (kBoth) return ft[k];
+            else return fh[k];
+        };
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
             if (hd(k)) fh[k] = dot(Q[rh(t - k)], Sc[k]);
-            if (tl(k)) ft[k] = dot(Q[rt(t + OFF - k)], Sp[k]);
+            if (tl(k)) tf(k) = dot(Q[rt(t + OFF - k)], Sp[k]);
         }
 #pragma unroll
         for (int o = LANES / 2; o > 0; o >>= 1)
 #pragma unroll
             for (int k = 0; k < NC; ++k) {
                 if (hd(k)) fh[k] += __shfl_xor_sync(kFull, fh[k], o);
-                if (tl(k)) ft[k] += __shfl_xor_sync(kFull, ft[k], o);
+                if (tl(k)) tf(k) += __shfl_xor_sync(kFull, tf(k), o);
             }
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
@@ -234,7 +241,7 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
             }
             if (tl(k)) {
                 const int jt = t + OFF - k;
-                update(Q[rt(jt)], Sp[k], coeff(ft[k], ((tvm >> rt(jt)) & 1u) ? nha : 0.0f, k == 0));
+                update(Q[rt(jt)], Sp[k], coeff(tf(k), ((tvm >> rt(jt)) & 1u) ? nha : 0.0f, k == 0));
                 if (jt == NCTX - 1) writeback(Sp[k], prv + k * STRIDE, __shfl_sync(kFull, idp, gl + k), tact);
             }
         }
@@ -243,7 +250,6 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     for (int i = 0; i < Lmax; ++i) {
         const bool act = i < L;
         const bool wact = act && L >= 2;
-        if (sub == 0 && act) obs_record(b, sent, i);
         const int q_in = i + 1 + WF;
         const float* cur = sbuf + (i & 1) * NC * STRIDE;
         const float* prv = sbuf + ((i + 1) & 1) * NC * STRIDE;

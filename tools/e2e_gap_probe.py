@@ -21,6 +21,13 @@ with fw.Trainer(cfg, corpus.counts) as t:
         print(f"epoch {it}: wall {dt * 1e3:.2f} ms, report wall {rep.wall_seconds * 1e3:.2f} ms, kernel span "
               f"{rep.kernel_seconds * 1e3:.2f} ms, {rep.words_trained / dt / 1e6:.1f} Mw/s, batching "
               f"{rep.batching_words_per_sec / 1e6:.1f} Mw/s/thread", flush=True)
+    import dataclasses
+    with fw.Trainer(dataclasses.replace(cfg, epochs=10), corpus.counts) as t10:
+        t10.train_corpus(corpus)
+        t0 = time.perf_counter()
+        rep = t10.train_corpus(corpus)
+        dt = time.perf_counter() - t0
+        print(f"10-epoch call: {dt * 1e3 / 10:.2f} ms/epoch, {rep.words_trained / dt / 1e6:.1f} Mw/s", flush=True)
     plan = t.plan_epoch(corpus, 0)
     for it in range(3):
         s, _ = plan.run()
