@@ -386,8 +386,10 @@ def config_block(args, shape, words, world, parallelism):
             "deviations": {"hot_rows": f"top {args.hot_rows} output rows trained as 16 replicas, merged as their "
                                        "mean after each pass (their step is 1/16 of plain Hogwild's; "
                                        "tests/test_quality.py::test_text8_hot_band_loss)" if args.hot_rows else "off",
-                           "l1_staging": f"sample rows staged through L1, refreshed every 2^{args.l1_refresh_log2} "
-                                         "windows per SM (other sentences' updates seen up to that late)",
+                           "l1_staging": (f"window-snapshot order: sample rows staged through L1, refreshed every "
+                                          f"2^{args.l1_refresh_log2} windows per SM (other sentences' updates seen up to "
+                                          "that late); lifetime order stages through L2 only (cp.async.cg): no staleness "
+                                          "beyond Hogwild's in-flight updates"),
                            "sigmoid": "tanh.approx (|err| < 1e-3, SPEC.md:252)"},
             "parallelism": parallelism,
             "l2_policy": "inputs (238 MB id/negative stream per step) > 126 MB L2; no flush"}

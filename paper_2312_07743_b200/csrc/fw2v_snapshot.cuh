@@ -220,12 +220,18 @@ struct Slice {
             else *reinterpret_cast<float2*>(p + c * CS) = make_float2(0.0f, 0.0f);
         }
     }
-    // Stage the lane's slice of a global row into shared memory (cp.async through L1).
+    // Stage the lane's slice of a global row into shared memory: through L1
+    // (cp.async.ca), or with L2ONLY through L2 alone (cp.async.cg, 16-byte chunks:
+    // every read sees every write that reached L2, the sentence's own included).
+    static constexpr bool kCanL2Only = CW == 4;
+    template <bool L2ONLY = false>
     __device__ __forceinline__ static void stage(float* dst, const float* src) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + c * CS));
-            if constexpr (CW == 4)
+            if constexpr (CW == 4 && L2ONLY)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
+            else if constexpr (CW == 4)
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * CS) : "memory");
             else
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + c * CS) : "memory");

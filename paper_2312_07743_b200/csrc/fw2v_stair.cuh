@@ -143,7 +143,7 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
             const int s = __shfl_sync(kFull, idw, gl + q);
-            if (s >= 0) SL::stage(dst + q * STRIDE, srow(s));
+            if (s >= 0) SL::template stage<true>(dst + q * STRIDE, srow(s));
         }
         cp_async_commit();
     };
@@ -306,8 +306,10 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
         }
         // (Next window's staging is issued after this window's tail steps.)
         auto issue_next = [&]() {
-            if (l1_exact || (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
-                             (threadIdx.x >> 5) == 0))
+            // Rows staged through L1 (8-byte chunks) need its refresh; with 16-byte
+            // chunks they come from L2 (cp.async.cg) and see every write there.
+            if (!SL::kCanL2Only && (l1_exact || (inval_mask != 0u && (static_cast<unsigned>(i) & inval_mask) == inval_mask &&
+                                                  (threadIdx.x >> 5) == 0)))
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
             const bool nact = i + 1 < L && L >= 2;
             idn = make_id(qtok[WF + 1], nr_next, nact);

@@ -83,22 +83,25 @@ def test_stair_equals_wavefront_bitwise(dim, window, types_per_band):
 
 @pytest.mark.parametrize("hot_rows", [0, 64])
 def test_stair_hogwild_text8_loss(ref, hot_rows):
-    """Hogwild epochs on the text8 shape (first 4,000 sentences, 2 epochs): the
-    staircase and the one-window wavefront (which differ only in Hogwild
-    interleaving) each reach the reference train()'s SGNS loss within 2%."""
+    """One Hogwild epoch on the text8 shape: the staircase and the one-window
+    wavefront (which differ only in Hogwild interleaving) each reach the reference
+    train()'s SGNS loss within 2%. (On a 4,000-sentence subset the reference's own
+    loss varied by 1.5% between runs of its 16 Hogwild threads; the whole corpus
+    keeps that spread well below the tolerance.)"""
     from oracle.oracle import TrainConfig as RConfig
 
-    corpus = fw.synth_zipf(**fw.TEXT8_SHAPE).head(4000)
-    base = dict(dim=128, window=5, negatives=5, epochs=2, batch_sentences=10000, subsample=1e-4, seed=3)
+    corpus = fw.synth_zipf(**fw.TEXT8_SHAPE)
+    base = dict(dim=128, window=5, negatives=5, epochs=1, batch_sentences=10000, subsample=1e-4, seed=3)
     p = corpus.counts.astype(np.float64) ** 0.75
-    negs = np.random.default_rng(5).choice(len(corpus.counts), len(corpus.ids) * 5, p=p / p.sum()).astype(np.int32)
+    off = corpus.offsets[:2001].copy()
+    negs = np.random.default_rng(5).choice(len(corpus.counts), int(off[-1]) * 5, p=p / p.sum()).astype(np.int32)
 
     def loss(i, o):
-        return sgns_loss(i, o, corpus.offsets, corpus.ids, negs, 3, 5, max_pairs=100_000)
+        return sgns_loss(i, o, off, corpus.ids[: int(off[-1])], negs, 3, 5, max_pairs=200_000)
 
     rin, rout, _ = ref.train(corpus.counts, corpus.offsets, corpus.ids, RConfig(workers=os.cpu_count() or 8, **base))
     ref_loss = loss(rin, rout)
-    cfg = fw.TrainConfig(workers=16, streams=4, deterministic=0, reuse_mode="lifetime", sampler="alias",
+    cfg = fw.TrainConfig(workers=64, streams=16, deterministic=0, reuse_mode="lifetime", sampler="alias",
                          hot_rows=hot_rows, **base)
     got = []
     for stair in (True, False):
