@@ -234,7 +234,8 @@ def make_config(fw, args, mode, local, seed=1, epochs=None, workers=None):
                           epochs=epochs or max(1, args.steps), workers=workers or args.chunks, streams=args.streams,
                           batch_sentences=args.batch_sentences, subsample=1e-4, seed=seed, deterministic=0,
                           reuse_mode=mode, device=local, sampler=args.sampler,
-                          l1_refresh_log2=args.l1_refresh_log2, k1_lanes=args.k1_lanes, hot_rows=args.hot_rows)
+                          l1_refresh_log2=args.l1_refresh_log2, k1_lanes=args.k1_lanes, hot_rows=args.hot_rows,
+                          hot_merge=args.hot_merge)
 
 
 def roofline(args, words, seconds, mode, prof):
@@ -301,12 +302,11 @@ def dropin_leg(fw, args, corpus):
         return {"unavailable": str(e)}
     out = {"path": "ringvec::train (C++ drop-in, libringvec_fw2v.so) per call: fw2v_create (tables, HBM model, "
                    "init_model), host batching, H2D, kernels, model readback; reference default TrainConfig "
-                   "(epochs=20, workers=0 -> hardware threads; alias sampler, no hot-row replicas, "
-                   "auto in-flight budget)"}
+                   "(epochs=20, workers=0 -> hardware threads; drop-in defaults: alias sampler, top-64 hot-row "
+                   "replicas with the live merge, auto in-flight budget)"}
     try:
-        # reference default; then FW2V_HOT_ROWS=64 (the bench's hot-row replicas: the top-64
-        # output rows' step is 1/16 of plain Hogwild's, which lets every sentence run at once)
-        for key, env in (("", {}), ("_hot_rows_64", {"FW2V_HOT_ROWS": "64"})):
+        # drop-in defaults; then without the hot-row replicas (plain Hogwild on every row)
+        for key, env in (("", {}), ("_no_hot_rows", {"FW2V_HOT_ROWS": "0"})):
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
             try:
@@ -383,9 +383,11 @@ def config_block(args, shape, words, world, parallelism):
             "streams": args.streams, "chunks": args.chunks, "reuse_mode": args.reuse_mode,
             "kernel": "K1s (FULL-W2V independent negatives, Hogwild)", "sampler": args.sampler,
             "l1_refresh_log2": args.l1_refresh_log2,
-            "deviations": {"hot_rows": f"top {args.hot_rows} output rows trained as 16 replicas, merged as their "
-                                       "mean after each pass (their step is 1/16 of plain Hogwild's; "
-                                       "tests/test_quality.py::test_text8_hot_band_loss)" if args.hot_rows else "off",
+            "deviations": {"hot_rows": (f"top {args.hot_rows} output rows trained as 16 replicas merged live (every "
+                                        "replica's updates summed into the others every few microseconds by a resident "
+                                        "merge block: plain Hogwild's step, tests/test_hot_live.py)" if args.hot_merge
+                                        else f"top {args.hot_rows} output rows trained as 16 replicas merged as their mean "
+                                        "after each pass (1/16 of plain Hogwild's step)") if args.hot_rows else "off",
                            "l1_staging": (f"window-snapshot order: sample rows staged through L1, refreshed every "
                                           f"2^{args.l1_refresh_log2} windows per SM (other sentences' updates seen up to "
                                           "that late); lifetime order stages through L2 only (cp.async.cg): no staleness "
@@ -557,6 +559,7 @@ def main():
     ap.add_argument("--l1-refresh-log2", type=int, default=5)
     ap.add_argument("--k1-lanes", type=int, default=0, help="lanes per sentence (0 = auto)")
     ap.add_argument("--hot-rows", type=int, default=64)
+    ap.add_argument("--hot-merge", type=int, default=1, help="1 live sum merge of the hot-row replicas, 0 pass-end mean")
     ap.add_argument("--average-words", type=int, default=25_000_000,
                     help="multi-GPU: merge the replicas every this many trained words per GPU")
     ap.add_argument("--ref-budget-s", type=float, default=200.0,

@@ -103,6 +103,10 @@ typedef struct fw2v_config {
                                  in magnitude: a Hogwild blow-up); if not, restore it,
                                  halve the in-flight budget and train the epoch again (up to 4 times,
                                  then FW2V_ERR_DIVERGED). 0 = off (no snapshot, no check) */
+    int32_t hot_merge;    /* hot-row replicas (hot_rows > 0): 1 = live: a resident merge block sums every
+                             replica's updates into the others every few microseconds during the pass, so
+                             the hot rows take plain Hogwild's full step (default); 0 = mean of the replicas
+                             at the end of each pass (each replica's updates count 1/hot_replicas) */
 } fw2v_config;
 
 enum fw2v_replica_merge { FW2V_MERGE_MEAN = 0, FW2V_MERGE_TOUCHED = 1, FW2V_MERGE_SUM = 2 };

@@ -50,6 +50,8 @@ cudaError_t launch_k2(const ModelView& m, const BatchView& b, int n_neg, int wf,
 cudaError_t launch_init_model(const ModelView& m, uint64_t state0, cudaStream_t st);
 // Hot-row replicas: average = false broadcasts syn1 rows 0..K-1 into them, true averages them back.
 cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st);
+cudaError_t launch_hot_live(const ModelView& m, int* stop, int* started, cudaStream_t st);
+cudaError_t launch_set_flag(int* f, cudaStream_t st);
 cudaError_t launch_nonfinite(const float* p, size_t n, int* flag, cudaStream_t st);
 // K1s family: window-snapshot order, or (lifetime = true) the reference's lifetime order as a wavefront.
 cudaError_t launch_k1s(int lanes, int vec, const ModelView& m, const BatchView& b, int n_neg, int wf, bool fast,
@@ -550,6 +552,9 @@ void validate(const fw2v_config& c) {  // validate_config (config.cpp:165-177)
     if (c.hot_rows < 0 || c.hot_replicas < 1) fail(FW2V_ERR_BAD_CONFIG, "hot_rows must be >= 0 and hot_replicas >= 1");
     if (c.delta_writeback < 0 || c.delta_writeback > 2) fail(FW2V_ERR_BAD_CONFIG, "delta_writeback must be 0, 1 or 2");
     if (c.replica_merge < 0 || c.replica_merge > 1) fail(FW2V_ERR_BAD_CONFIG, "replica_merge must be 0 or 1");
+    if (c.hot_merge < 0 || c.hot_merge > 1) fail(FW2V_ERR_BAD_CONFIG, "hot_merge must be 0 or 1");
+    if (c.hot_merge == 1 && c.hot_rows > 0 && c.hot_replicas > 16)
+        fail(FW2V_ERR_BAD_CONFIG, "the live hot-row merge takes at most 16 replicas");
 }
 
 void require_device(int device) {
@@ -763,6 +768,51 @@ struct fw2v_ctx {
     }
     // Around every Hogwild pass: replicas <- syn1 before, syn1 <- mean(replicas) after.
     void hot_sync(bool average, cudaStream_t st) const { FW2V_CK(launch_hot_sync(model_view(), average, st)); }
+    // Live merge (cfg.hot_merge = 1): a resident merge block runs beside the pass's
+    // training kernels (k_hot_live) on its own stream.
+    cudaStream_t live_stream = nullptr;
+    cudaEvent_t live_go = nullptr, live_done = nullptr;
+    int* live_stop = nullptr;        // device flag
+    int* live_started_h = nullptr;   // mapped host flag, set by the merge block
+    int* live_started_d = nullptr;
+    bool live() const { return cfg.hot_merge == 1 && hot_k > 0 && !deterministic; }
+    // Before a pass (on stream st, before any training kernel is queued): replicas <-
+    // syn1; with the live merge, start the merge block and wait until it is resident
+    // (so it cannot be starved behind the pass's kernels).
+    void hot_begin(cudaStream_t st) {
+        hot_sync(false, st);
+        if (!live()) return;
+        if (live_stream == nullptr) {
+            FW2V_CK(cudaStreamCreateWithFlags(&live_stream, cudaStreamNonBlocking));
+            FW2V_CK(cudaEventCreateWithFlags(&live_go, cudaEventDisableTiming));
+            FW2V_CK(cudaEventCreateWithFlags(&live_done, cudaEventDisableTiming));
+            FW2V_CK(cudaMalloc(&live_stop, sizeof(int)));
+            FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&live_started_h), sizeof(int), cudaHostAllocMapped));
+            FW2V_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&live_started_d), live_started_h, 0));
+        }
+        *reinterpret_cast<volatile int*>(live_started_h) = 0;
+        FW2V_CK(cudaMemsetAsync(live_stop, 0, sizeof(int), st));
+        FW2V_CK(cudaEventRecord(live_go, st));
+        FW2V_CK(cudaStreamWaitEvent(live_stream, live_go, 0));
+        FW2V_CK(launch_hot_live(model_view(), live_stop, live_started_d, live_stream));
+        FW2V_CK(cudaEventRecord(live_done, live_stream));
+        const double t0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+        while (*reinterpret_cast<volatile int*>(live_started_h) == 0) {
+            const double t = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+            if (t - t0 > 5.0) fail(FW2V_ERR_CUDA, "live hot-row merge block did not start");
+            std::this_thread::yield();
+        }
+    }
+    // After a pass (st has joined every training stream): the mean of the replicas
+    // back into syn1, or stop the live merge and wait for its final sweep.
+    void hot_end(cudaStream_t st) {
+        if (!live()) {
+            hot_sync(true, st);
+            return;
+        }
+        FW2V_CK(launch_set_flag(live_stop, st));
+        FW2V_CK(cudaStreamWaitEvent(st, live_done, 0));
+    }
 
     Sampler sampler() const {
         Sampler s;
@@ -901,6 +951,14 @@ struct fw2v_ctx {
         cudaFree(merge_cnt);
         cudaFree(guard_snap);
         cudaFree(guard_flag);
+        if (live_stream) {
+            cudaStreamSynchronize(live_stream);
+            cudaStreamDestroy(live_stream);
+            cudaEventDestroy(live_go);
+            cudaEventDestroy(live_done);
+            cudaFree(live_stop);
+            cudaFreeHost(live_started_h);
+        }
         cudaFree(hot_alloc);
         if (own_model) {
             cudaFree(syn0);
@@ -1015,6 +1073,7 @@ void fw2v_config_default(fw2v_config* c) {
     c->hot_replicas = 16;
     c->replica_merge = FW2V_MERGE_TOUCHED;
     c->divergence_guard = 1;
+    c->hot_merge = 1;
 }
 
 int fw2v_validate_config(const fw2v_config* cfg) {
@@ -1090,7 +1149,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
             x->place_hot();
             x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
                                 : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives,
-                                                                         cfg->alpha0, x->hot_k, x->hot_r, cfg->dim)
+                                                                         cfg->alpha0, x->live() ? 0 : x->hot_k, x->hot_r, cfg->dim)
                                                          : 0;
         }
         if (x->inflight_total > 0 && !x->deterministic) {
@@ -1218,9 +1277,9 @@ int fw2v_train_sentences(fw2v_ctx* x, const uint64_t* offsets, uint64_t n_senten
         FW2V_CK(cudaMemcpy(d_off, off.data(), 4 * (n_sentences + 1), cudaMemcpyHostToDevice));
         if (n_sentences) FW2V_CK(cudaMemcpy(d_alpha, alphas, 4 * n_sentences, cudaMemcpyHostToDevice));
         BatchView bv{d_ids, d_off, d_negs, d_alpha, static_cast<int32_t>(n_sentences)};
-        if (!serial) x->hot_sync(false, nullptr);
+        if (!serial && x->hot_k > 0) x->hot_begin(nullptr);
         FW2V_CK(x->launch(bv, serial != 0, d_ctr, nullptr));
-        if (!serial) x->hot_sync(true, nullptr);
+        if (!serial && x->hot_k > 0) x->hot_end(nullptr);
         FW2V_CK(cudaDeviceSynchronize());
         DevCounters h{};
         FW2V_CK(cudaMemcpy(&h, d_ctr, sizeof(h), cudaMemcpyDeviceToHost));
@@ -1341,7 +1400,7 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
     // kernel stream starts after them.
     FW2V_CK(cudaEventRecord(ev.t0, s0));
     for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), s0));
-    if (hot) x->hot_sync(false, s0);
+    if (hot) x->hot_begin(s0);
     FW2V_CK(cudaEventRecord(ev.synced, s0));
     for (int p = 0; p < P; ++p) {
         if (p > 0) FW2V_CK(cudaStreamWaitEvent(x->lanes[static_cast<size_t>(p)].stream, ev.synced, 0));
@@ -1592,7 +1651,7 @@ void run_pass(fw2v_ctx* x, const CorpusView& corpus, const std::vector<ChunkSpan
         FW2V_CK(cudaEventRecord(ev.join[static_cast<size_t>(2 * p + 1)], ln.stream2));
         FW2V_CK(cudaStreamWaitEvent(s0, ev.join[static_cast<size_t>(2 * p + 1)], 0));
     }
-    if (hot) x->hot_sync(true, s0);
+    if (hot) x->hot_end(s0);
     FW2V_CK(cudaEventRecord(ev.t1, s0));
     FW2V_CK(cudaEventSynchronize(ev.t1));
     float ms = 0.0f;
@@ -2279,7 +2338,7 @@ int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* 
         for (int p = 0; p < P; ++p) FW2V_CK(cudaMemsetAsync(x->lanes[static_cast<size_t>(p)].d_ctr, 0, sizeof(DevCounters), s0));
         FW2V_CK(cudaEventRecord(start, s0));
         const bool hot = !x->deterministic && x->hot_k > 0;
-        if (hot) x->hot_sync(false, s0);
+        if (hot) x->hot_begin(s0);
         FW2V_CK(cudaEventRecord(fork, s0));
         const int KS = x->kernel_streams();
         for (int p = 0; p < P; ++p) {
@@ -2306,7 +2365,7 @@ int fw2v_plan_run(fw2v_ctx* x, fw2v_plan* plan, double* seconds, fw2v_counters* 
         if (hot) {
             // Join every lane on s0, fold the replicas back; the pass ends there.
             for (int p = 1; p < P; ++p) FW2V_CK(cudaStreamWaitEvent(s0, ends[static_cast<size_t>(p)], 0));
-            x->hot_sync(true, s0);
+            x->hot_end(s0);
             FW2V_CK(cudaEventRecord(ends[0], s0));
         }
         float ms_max = 0.0f;

@@ -653,6 +653,71 @@ __global__ void k_hot_average(ModelView m) {
         m.syn1[x] = s * inv;
     }
 }
+// Live hot-row merge (fw2v_config.hot_merge = 1): one resident block keeps the
+// base (syn1 rows 0..K-1) equal to the sum of every replica's updates and hands
+// each replica the others' updates, sweeping until *stop: replica r gets
+// red.add(D - d_r) with d_r = its own change since the last sweep and D = the sum
+// over replicas, so an update reaches every replica within a sweep (~µs, like a
+// plain Hogwild update reaching L2) and the hot rows take plain Hogwild's full
+// step instead of the mean's 1/R. red.add keeps updates that land between the
+// sweep's read and its write. *started tells the host the block is resident.
+constexpr int kMaxLiveReplicas = 16;
+__global__ void __launch_bounds__(512) k_hot_live(ModelView m, const volatile int* stop, volatile int* started,
+                                                  unsigned sleep_ns, unsigned long long max_ns) {
+    const int n4 = m.hot_k * m.stride / 4;
+    float4* base = reinterpret_cast<float4*>(m.syn1);
+    float4* rep = reinterpret_cast<float4*>(m.hot);
+    const int R = m.hot_r;
+    __shared__ int last;
+    unsigned long long t0 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (threadIdx.x == 0) *started = 1;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            last = (*stop != 0) || (t - t0 > max_ns);  // (time cap: never outlive a lost stop)
+        }
+        __syncthreads();
+        const bool fin = last != 0;
+        for (int x = threadIdx.x; x < n4; x += blockDim.x) {
+            const float4 b = __ldcg(base + x);
+            float4 d[kMaxLiveReplicas];
+            float4 D = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+            for (int r = 0; r < kMaxLiveReplicas; ++r) {
+                if (r < R) {
+                    const float4 v = __ldcg(rep + static_cast<size_t>(r) * n4 + x);
+                    d[r] = make_float4(v.x - b.x, v.y - b.y, v.z - b.z, v.w - b.w);
+                    D.x += d[r].x; D.y += d[r].y; D.z += d[r].z; D.w += d[r].w;
+                }
+            }
+            if (D.x == 0.0f && D.y == 0.0f && D.z == 0.0f && D.w == 0.0f) continue;
+#pragma unroll
+            for (int r = 0; r < kMaxLiveReplicas; ++r) {
+                if (r < R)
+                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(rep + static_cast<size_t>(r) * n4 + x),
+                                 "f"(D.x - d[r].x), "f"(D.y - d[r].y), "f"(D.z - d[r].z), "f"(D.w - d[r].w)
+                                 : "memory");
+            }
+            __stcg(base + x, make_float4(b.x + D.x, b.y + D.y, b.z + D.z, b.w + D.w));
+        }
+        __syncthreads();
+        if (fin) break;
+        __nanosleep(sleep_ns);
+    }
+}
+__global__ void k_set_flag(int* f) { *f = 1; }
+cudaError_t launch_hot_live(const ModelView& m, int* stop, int* started, cudaStream_t st) {
+    if (m.hot_k <= 0 || m.hot_r > kMaxLiveReplicas) return cudaErrorInvalidValue;
+    k_hot_live<<<1, 512, 0, st>>>(m, stop, started, 2000u, 30ull * 1000 * 1000 * 1000);
+    return cudaGetLastError();
+}
+cudaError_t launch_set_flag(int* f, cudaStream_t st) {
+    k_set_flag<<<1, 1, 0, st>>>(f);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_hot_sync(const ModelView& m, bool average, cudaStream_t st) {
     if (m.hot_k <= 0) return cudaSuccess;
     const int n = m.hot_k * m.stride;

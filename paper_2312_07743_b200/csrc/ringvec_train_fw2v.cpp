@@ -109,11 +109,13 @@ TrainResult train(const Corpus& corpus, const TrainConfig& raw_config, TrainObse
     c.l1_refresh_log2 = env_int("FW2V_L1_REFRESH_LOG2", c.l1_refresh_log2);
     c.delta_writeback = env_int("FW2V_DELTA_WRITEBACK", c.delta_writeback);
     c.max_inflight = env_int("FW2V_MAX_INFLIGHT", c.max_inflight);
-    // Hot-row replicas change the update rule of the most frequent output rows
-    // (each replica sees 1/R of the sentences; merged as their mean), so the
-    // drop-in keeps plain Hogwild unless FW2V_HOT_ROWS asks for them.
-    c.hot_rows = env_int("FW2V_HOT_ROWS", 0);
+    // Hot-row replicas spread the L2 reductions on the most frequent output rows;
+    // the live merge (hot_merge = 1) hands every replica the others' updates within
+    // microseconds, so the rows keep plain Hogwild's update rule (full step).
+    // FW2V_HOT_MERGE=0 selects round 1's pass-end mean (1/R step on those rows).
+    c.hot_rows = env_int("FW2V_HOT_ROWS", c.hot_rows);
     c.hot_replicas = env_int("FW2V_HOT_REPLICAS", c.hot_replicas);
+    c.hot_merge = env_int("FW2V_HOT_MERGE", c.hot_merge);
 
     std::vector<uint64_t> counts(static_cast<size_t>(vocab.size()));
     for (int32_t w = 0; w < vocab.size(); ++w) counts[static_cast<size_t>(w)] = vocab.entry(w).count;

@@ -70,7 +70,7 @@ class CConfig(C.Structure):
         ("fast_sigmoid", C.c_int32), ("k1_lanes", C.c_int32), ("streams", C.c_int32),
         ("l1_refresh_log2", C.c_int32), ("delta_writeback", C.c_int32), ("max_inflight", C.c_int32),
         ("hot_rows", C.c_int32), ("hot_replicas", C.c_int32), ("replica_merge", C.c_int32),
-        ("divergence_guard", C.c_int32),
+        ("divergence_guard", C.c_int32), ("hot_merge", C.c_int32),
     ]
 
 
@@ -137,6 +137,7 @@ class TrainConfig:
     hot_replicas: int = 16
     replica_merge: str = "touched"  # data-parallel rounds: mean | touched (include/fw2v.h)
     divergence_guard: int = 1  # Hogwild: finite check per epoch, restore + halve in-flight on failure
+    hot_merge: int = 1  # hot-row replicas: 1 live sum (full Hogwild step), 0 mean at the end of each pass
 
     @property
     def context_width(self) -> int:
