@@ -789,6 +789,14 @@ struct fw2v_ctx {
             FW2V_CK(cudaMalloc(&live_stop, sizeof(int)));
             FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&live_started_h), sizeof(int), cudaHostAllocMapped));
             FW2V_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&live_started_d), live_started_h, 0));
+            // Every kernel the pass launches while the merge block runs is loaded now:
+            // with lazy module loading a first launch can wait for the running
+            // kernels, i.e. for the merge block that waits for it (the stop-flag
+            // kernel, the training kernel).
+            FW2V_CK(launch_set_flag(live_stop, st));
+            int resident = 0;
+            FW2V_CK(launch_one(BatchView{}, false, nullptr, nullptr, &resident));
+            FW2V_CK(cudaStreamSynchronize(st));
         }
         *reinterpret_cast<volatile int*>(live_started_h) = 0;
         FW2V_CK(cudaMemsetAsync(live_stop, 0, sizeof(int), st));
