@@ -518,6 +518,9 @@ Shape choose_shape(int dim, int lanes_pref) {
 // (registers), up to 16 on 32 lanes for wide rows (d = 300 -> 32 x 10); d = 512 runs on two
 // warps per sentence (64 x 8).
 Shape choose_k1s_shape(int stride, const Shape& k1, int lanes_pref, int n_neg, int wf, bool lifetime) {
+    // Lifetime order with N = 15: the staircase streams the 16 samples on 32-lane
+    // groups (the repeat check needs 2 x 16 lanes), at 4 columns per lane.
+    if (lanes_pref == 0 && lifetime && n_neg == 15 && wf <= 3 && stride == 128) return Shape{32, 4};
     if (lanes_pref == 0) {
         static const Shape pref[] = {{4, 4}, {8, 4}, {16, 4}, {16, 8}, {32, 4}, {32, 6}, {32, 8}, {32, 10}, {32, 12},
                                      {64, 8}, {32, 16}};

@@ -959,6 +959,13 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
     constexpr int per_block = K1sSmem<LANES, VEC, WF, NC>::THREADS / LANES;  // RING does not change THREADS
     const int blocks = k1s_grid(b, per_block);
     if (n_neg + 1 > NC) {
+        // Lifetime order, N = 15 on 32-lane groups: the staircase with the 16
+        // samples streaming through 2W_f register slots (one wavefront per window).
+        // (4 columns per lane: at 8 the 17-step unrolled iteration no longer fits.)
+        if constexpr (NC == 6 && LANES == 32 && WF <= 3 && VEC == 4) {
+            if (lifetime && n_neg + 1 == 16 && fast && (m.flags & kFlagNoRing) != 0 && (m.flags & kFlagNoStair) == 0)
+                return launch_k1s_stair<LANES, VEC, WF, 16, true>(m, b, ctr, st, resident);
+        }
         // Chunks of NC samples; in lifetime order each chunk is its own wavefront,
         // started from the contexts the previous chunk left (exact order).
         if constexpr (VEC <= 10) {
@@ -986,7 +993,7 @@ cudaError_t launch_k1s_nc(const ModelView& m, const BatchView& b, int n_neg, boo
         if constexpr (NC == 6 && (LANES == 16 || LANES == 32) && WF <= 5 && (VEC == 4 || VEC == 8 || VEC == 10) &&
                       (WF <= 3 || VEC != 10)) {
             if (lifetime && fast && (m.flags & kFlagNoRing) != 0 && (m.flags & kFlagNoStair) == 0)
-                return launch_k1s_stair<LANES, VEC, WF, true>(m, b, ctr, st, resident);
+                return launch_k1s_stair<LANES, VEC, WF, 6, true>(m, b, ctr, st, resident);
         }
         return lifetime ? launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, true>(blocks, m, b, n_neg, fast, ctr, st, resident)
                         : launch_k1s_mode<LANES, VEC, WF, NC, kFullChunk, false>(blocks, m, b, n_neg, fast, ctr, st, resident);

@@ -33,10 +33,14 @@
 
 namespace fw2v {
 
-template <int LANES, int VEC, int WF>
+template <int LANES, int VEC, int WF, int NS_ = 6>
 struct StairCfg {
-    static constexpr int NC = 6;                       // samples per window (N = 5)
+    static constexpr int NC = NS_;                     // samples per window (N + 1)
     static constexpr int NCTX = 2 * WF;
+    // Sample rows in registers per window: a sample is live for 2W_f consecutive
+    // steps (its pairings with the contexts), so at most 2W_f are live at once;
+    // sample k lives in slot k mod NSL (N + 1 = 16 runs through 6 slots at W_f = 3).
+    static constexpr int NSL = NC < NCTX ? NC : NCTX;
     static constexpr int NQ = 2 * WF + 1;              // ring rows in registers
     static constexpr int STEPS_ = NC + 2 * WF - 1;
     // Window-to-window offset in steps: >= NC + 1 (the first sample of window i+1
@@ -63,11 +67,12 @@ struct StairCfg {
 // LANES in {16, 32} (a group is half a warp or a warp; the repeat check uses
 // lanes 0..5 and HALF..HALF+5 of the group), N = 5, Hogwild overwrite of the
 // context rows.
-template <int LANES, int VEC, int WF, bool FAST>
+template <int LANES, int VEC, int WF, int NS, bool FAST>
 __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchView& b, DevCounters* __restrict__ ctr,
                                                int sent0) {
-    using CF = StairCfg<LANES, VEC, WF>;
-    constexpr int NC = CF::NC, NN = NC - 1, NCTX = CF::NCTX, NQ = CF::NQ, OFF = CF::OFF, T = CF::T;
+    using CF = StairCfg<LANES, VEC, WF, NS>;
+    constexpr int NC = CF::NC, NN = NC - 1, NCTX = CF::NCTX, NQ = CF::NQ, OFF = CF::OFF, T = CF::T, NSL = CF::NSL;
+    auto sl_ = [](int k) { return k % NSL; };  // register slot of sample k
     constexpr int H2 = VEC / 2;
     constexpr int STRIDE = CF::STRIDE;
     constexpr int HALF = LANES / 2;
@@ -199,9 +204,9 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     auto rh = [](int j) { return j < WF ? j : j + 1; };
     auto rt = [](int j) { return j < WF ? j - 1 : j; };
 
-    float2 Sc[NC][H2], Sp[NC][H2];
+    float2 Sc[NSL][H2], Sp[NSL][H2];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) { vzero2(Sc[k]); vzero2(Sp[k]); }
+    for (int k = 0; k < NSL; ++k) { vzero2(Sc[k]); vzero2(Sp[k]); }
     bool tact = false;  // the previous window's tail is pending
     unsigned tvm = 0;   // tail validity per ring row (previous window, current indexing)
 
@@ -211,10 +216,11 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     auto step = [&](const int t, const bool HEAD, unsigned hvm, const float* cur, const float* prv, bool wact) {
         auto hd = [&](int k) { return HEAD && t - k >= 0 && t - k < NCTX; };
         auto tl = [&](int k) { return t + OFF - k >= 0 && t + OFF - k < NCTX; };
-        // Up to W_f = 3 a sample index has at most one pairing per step (head rows
-        // k <= t, tail rows k >= t + 2): one dot array. At W_f >= 4 it can have
-        // both (rows Sc[k] and Sp[k]): a second array for the tail.
-        constexpr bool kBoth = NCTX > NC + 1;
+        // Head samples are k <= t, tail samples k >= t + OFF - NCTX + 1: while
+        // OFF >= NCTX a sample index has at most one pairing per step (one dot
+        // array); otherwise (W_f >= 4 at N = 5) it can have both (slots of Sc and
+        // Sp): a second array for the tail.
+        constexpr bool kBoth = OFF < NCTX;
         float fh[NC], ft[kBoth ? NC : 1];
         auto tf = [&](int k) -> float& {
             if constexpr (kBoth) return ft[k];
@@ -222,8 +228,8 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
         };
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            if (hd(k)) fh[k] = dot(Q[rh(t - k)], Sc[k]);
-            if (tl(k)) tf(k) = dot(Q[rt(t + OFF - k)], Sp[k]);
+            if (hd(k)) fh[k] = dot(Q[rh(t - k)], Sc[sl_(k)]);
+            if (tl(k)) tf(k) = dot(Q[rt(t + OFF - k)], Sp[sl_(k)]);
         }
 #pragma unroll
         for (int o = LANES / 2; o > 0; o >>= 1)
@@ -236,13 +242,13 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
         for (int k = 0; k < NC; ++k) {
             if (hd(k)) {
                 const int jh = t - k;
-                update(Q[rh(jh)], Sc[k], coeff(fh[k], ((hvm >> rh(jh)) & 1u) ? nha : 0.0f, k == 0));
-                if (jh == NCTX - 1) writeback(Sc[k], cur + k * STRIDE, __shfl_sync(kFull, idc, gl + k), wact);
+                update(Q[rh(jh)], Sc[sl_(k)], coeff(fh[k], ((hvm >> rh(jh)) & 1u) ? nha : 0.0f, k == 0));
+                if (jh == NCTX - 1) writeback(Sc[sl_(k)], cur + k * STRIDE, __shfl_sync(kFull, idc, gl + k), wact);
             }
             if (tl(k)) {
                 const int jt = t + OFF - k;
-                update(Q[rt(jt)], Sp[k], coeff(tf(k), ((tvm >> rt(jt)) & 1u) ? nha : 0.0f, k == 0));
-                if (jt == NCTX - 1) writeback(Sp[k], prv + k * STRIDE, __shfl_sync(kFull, idp, gl + k), tact);
+                update(Q[rt(jt)], Sp[sl_(k)], coeff(tf(k), ((tvm >> rt(jt)) & 1u) ? nha : 0.0f, k == 0));
+                if (jt == NCTX - 1) writeback(Sp[sl_(k)], prv + k * STRIDE, __shfl_sync(kFull, idp, gl + k), tact);
             }
         }
     };
@@ -318,45 +324,46 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
             mm_n = repeats_issue(idn, idc);
         };
         if (!dup) {
-            // Sample rows enter one step before their first pairing.
-            SL::load_shared(Sc[0], cur);
+            // Sample t enters its slot at step t (its first pairing): the slot's
+            // previous sample, t - NSL, had its last pairing at step t - 1.
 #pragma unroll
             for (int t = 0; t < OFF; ++t) {
-                if (t + 1 < NC) SL::load_shared(Sc[t + 1], cur + (t + 1) * STRIDE);
+                if (t < NC) SL::load_shared(Sc[sl_(t)], cur + t * STRIDE);
                 step(t, true, hvm, cur, prv, wact);
                 if (t == T) issue_next();
             }
-            // Rows k >= OFF - NCTX + 1 finish in the next iteration's tail.
+            // Samples k >= OFF - NCTX + 1 finish in the next iteration's tail.
 #pragma unroll
-            for (int k = 0; k < NC; ++k) vcopy2(Sp[k], Sc[k]);
+            for (int k = 0; k < NSL; ++k) vcopy2(Sp[k], Sc[k]);
             tvm = hvm;
             tact = wact && T > 0;
         } else {
             // Reference order, sample by sample; a repeated id starts from the
-            // row its previous occurrence left (the reference re-reads it).
-            int sidc[NC];
-#pragma unroll
-            for (int k = 0; k < NC; ++k) sidc[k] = __shfl_sync(kFull, idc, gl + k);
-#pragma unroll
+            // row its previous occurrence left (the reference re-reads it): that
+            // row is handed to the next occurrence through its staging slot, and
+            // the last occurrence writes final - staged (the first occurrence's
+            // slot keeps the staged row). Rare: a rolled loop, one row in registers.
+            const unsigned mmw = __match_any_sync(kFull, idc);  // lanes holding the same id
+            const unsigned grp_mask = (NC >= 32 ? ~0u : ((1u << NC) - 1u));
+#pragma unroll 1
             for (int k = 0; k < NC; ++k) {
-                SL::load_shared(Sc[k], cur + k * STRIDE);
-#pragma unroll
-                for (int k2 = 0; k2 < k; ++k2)
-                    if (sidc[k2] == sidc[k]) vcopy2(Sc[k], Sc[k2]);
+                float2 S[H2];
+                SL::load_shared(S, cur + k * STRIDE);
 #pragma unroll
                 for (int j = 0; j < NCTX; ++j) {
-                    float f = dot(Q[rh(j)], Sc[k]);
+                    float f = dot(Q[rh(j)], S);
 #pragma unroll
                     for (int o = LANES / 2; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
-                    update(Q[rh(j)], Sc[k], coeff(f, ((hvm >> rh(j)) & 1u) ? nha : 0.0f, k == 0));
+                    update(Q[rh(j)], S, coeff(f, ((hvm >> rh(j)) & 1u) ? nha : 0.0f, k == 0));
                 }
-            }
-#pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                bool last_occ = true;
-#pragma unroll
-                for (int q2 = q + 1; q2 < NC; ++q2) last_occ &= sidc[q2] != sidc[q];
-                writeback(Sc[q], cur + q * STRIDE, sidc[q], wact && last_occ);
+                const unsigned same = (__shfl_sync(kFull, mmw, gl + k) >> gl) & grp_mask;  // bit q: sample q
+                const int sid = __shfl_sync(kFull, idc, gl + k);  // (shuffles before the per-sentence branch)
+                const unsigned later = same & ~((2u << k) - 1u);
+                if (later != 0u) {
+                    SL::store_shared(const_cast<float*>(cur) + (__ffs(later) - 1) * STRIDE, S);
+                } else {
+                    writeback(S, cur + (__ffs(same) - 1) * STRIDE, sid, wact);
+                }
             }
             issue_next();
             tact = false;
@@ -422,19 +429,19 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
 }
 
 // Blocks stride over the batch's sentences (BatchView::max_groups caps the grid).
-template <int LANES, int VEC, int WF, bool FAST>
-__global__ void __launch_bounds__(StairCfg<LANES, VEC, WF>::THREADS, StairCfg<LANES, VEC, WF>::MINB)
+template <int LANES, int VEC, int WF, int NS, bool FAST>
+__global__ void __launch_bounds__(StairCfg<LANES, VEC, WF, NS>::THREADS, StairCfg<LANES, VEC, WF, NS>::MINB)
 k1s_stair(ModelView m, BatchView b, DevCounters* __restrict__ ctr) {
-    constexpr int PB = StairCfg<LANES, VEC, WF>::THREADS / LANES;
+    constexpr int PB = StairCfg<LANES, VEC, WF, NS>::THREADS / LANES;
     for (int s0 = static_cast<int>(blockIdx.x) * PB; s0 < b.n_sentences; s0 += static_cast<int>(gridDim.x) * PB)
-        stair_sentence<LANES, VEC, WF, FAST>(m, b, ctr, s0);
+        stair_sentence<LANES, VEC, WF, NS, FAST>(m, b, ctr, s0);
 }
 
-template <int LANES, int VEC, int WF, bool FAST>
+template <int LANES, int VEC, int WF, int NS, bool FAST>
 cudaError_t launch_k1s_stair(const ModelView& m, const BatchView& b, DevCounters* ctr, cudaStream_t st, int* resident) {
-    using CF = StairCfg<LANES, VEC, WF>;
+    using CF = StairCfg<LANES, VEC, WF, NS>;
     constexpr int bytes = CF::kBlockBytes;
-    auto* kern = k1s_stair<LANES, VEC, WF, FAST>;
+    auto* kern = k1s_stair<LANES, VEC, WF, NS, FAST>;
     static std::atomic<uint64_t> configured{0};
     if (cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), bytes, configured); e != cudaSuccess)
         return e;

@@ -203,11 +203,13 @@ def test_k1s_disjoint_batch_equals_serial(oracle, dim, delta):
 
 
 @pytest.mark.parametrize("replicas", [1, 2, 4])
-def test_k1s_hot_replicas_average(oracle, replicas):
+@pytest.mark.parametrize("hot_merge", [0, 1], ids=["mean", "live"])
+def test_k1s_hot_replicas_average(oracle, replicas, hot_merge):
     """Hot-row replicas: rows < hot_rows are trained by sentence s on replica
-    s mod R and averaged after the pass. With one sentence, its replica holds
-    the reference update and the other R-1 replicas the untouched rows, so
-    hot output rows end at v0 + (v_ref - v0) / R; everything else is exact."""
+    s mod R. With one sentence its replica holds the reference update and the
+    other R-1 replicas the untouched rows: the pass-end mean (hot_merge = 0)
+    leaves hot output rows at v0 + (v_ref - v0) / R, the live merge (1) at the
+    reference update itself; everything else is exact either way."""
     dim, n_neg, hot = 128, 5, 20
     counts, offsets, ids = random_corpus(1, 60, 40, seed=11, min_len=60)
     V = len(counts)
@@ -219,12 +221,13 @@ def test_k1s_hot_replicas_average(oracle, replicas):
     gi0, go0 = ri.copy(), ro.copy()
     oracle.train_sentences(ri, ro, offsets, ids, negs, alphas, OConfig(**cfg))
     with _trainer(counts=counts, deterministic=0, fast_sigmoid=False, l1_refresh_log2=0, delta_writeback=False,
-                  hot_rows=hot, hot_replicas=replicas, **cfg) as t:
+                  hot_rows=hot, hot_replicas=replicas, hot_merge=hot_merge, **cfg) as t:
         t.set_model(gi0, go0)
         t.train_sentences(offsets, ids, negs, alphas, serial=False)
         gi, go = t.get_model()
     want = ro.copy()
-    want[:hot] = go0[:hot] + (ro[:hot] - go0[:hot]) / replicas
+    if hot_merge == 0:
+        want[:hot] = go0[:hot] + (ro[:hot] - go0[:hot]) / replicas
     assert np.abs(gi - ri).max() <= 2e-5 * np.abs(ri).max() + 1e-7
     assert np.abs(go - want).max() <= 2e-5 * np.abs(ro).max() + 1e-7
 

@@ -120,3 +120,42 @@ def test_stair_hogwild_text8_loss(ref, hot_rows):
     print(f"hot_rows={hot_rows}: loss stair {got[0]:.4f} wavefront {got[1]:.4f} reference {ref_loss:.4f}")
     for g in got:
         assert abs(g - ref_loss) / ref_loss <= 0.02
+
+
+@pytest.mark.parametrize("types", [40, 2000], ids=["repeats", "rare"])
+def test_stair_n15_per_sentence_vs_oracle(oracle, types):
+    """N = 15 in lifetime order: the 16 samples stream through 2W_f register
+    slots of the staircase (32-lane groups, 32 x 4 at d=128). One sentence per
+    launch against the oracle's reference order (trainer.cpp:133-154), fast
+    sigmoid: relative update error <= 1e-4 (repeated ids inside a window take the
+    serial path with the row handed over, as the reference re-reads it)."""
+    from oracle.oracle import TrainConfig as OConfig
+
+    dim, n_neg, L, n = 128, 15, 120, 6
+    rng = np.random.default_rng(types)
+    V = max(types, 64)
+    counts = (10 + V - np.arange(V)).astype(np.uint64)
+    ids = rng.integers(0, types, n * L).astype(np.int32)
+    offsets = (np.arange(n + 1) * L).astype(np.uint64)
+    negs = rng.integers(0, types, n * L * n_neg).astype(np.int32)
+    alphas = np.full(n, 0.025, np.float32)
+    cfg = dict(dim=dim, window=5, negatives=n_neg, workers=4, reuse_mode="lifetime")
+    ri = ((rng.random((V, dim)) - 0.5) / dim).astype(np.float32)
+    ro = ((rng.random((V, dim)) - 0.5) * 0.5).astype(np.float32)
+    gi0, go0 = ri.copy(), ro.copy()
+    for s in range(n):
+        o = offsets[s:s + 2] - offsets[s]
+        oracle.train_sentences(ri, ro, o, ids[s * L:(s + 1) * L], negs[s * L * n_neg:(s + 1) * L * n_neg],
+                               alphas[s:s + 1], OConfig(**cfg))
+    with fw.Trainer(fw.TrainConfig(deterministic=0, hot_rows=0, fast_sigmoid=True, delta_writeback=2,
+                                   l1_refresh_log2=0, **cfg), counts) as t:
+        t.set_model(gi0, go0)
+        for s in range(n):
+            o = offsets[s:s + 2] - offsets[s]
+            t.train_sentences(o, ids[s * L:(s + 1) * L], negs[s * L * n_neg:(s + 1) * L * n_neg], alphas[s:s + 1],
+                              serial=False)
+        gi, go = t.get_model()
+    ei = np.linalg.norm((gi - ri).astype(np.float64)) / np.linalg.norm((ri - gi0).astype(np.float64))
+    eo = np.linalg.norm((go - ro).astype(np.float64)) / np.linalg.norm((ro - go0).astype(np.float64))
+    print(f"N=15 lifetime {types} types: relative update error input {ei:.2e} output {eo:.2e}")
+    assert ei <= 1e-4 and eo <= 1e-4
