@@ -59,7 +59,10 @@ struct StairCfg {
 #ifdef FW2V_STAIR_REG_BLOCKS  // experiments (tools/variant_lib.sh)
     static constexpr int kRegBlocks = FW2V_STAIR_REG_BLOCKS;
 #else
-    static constexpr int kRegBlocks = VEC < 8 ? 3 : 4;
+    // 16 x 8 at W_f <= 3: 5 blocks of 2 warps (168 registers, 28 B of spills) beat
+    // 4 blocks at 222 registers by 8% (profiles/r02bb_stair_blocks.txt); wider
+    // windows spill 0.7-1.2 KB at 168 and keep 4.
+    static constexpr int kRegBlocks = VEC < 8 ? 3 : (VEC == 8 && LANES == 16 && WF <= 3 && NS_ <= 6 ? 5 : 4);
 #endif
     static constexpr int MINB = kSmemBlocks < kRegBlocks ? (kSmemBlocks < 1 ? 1 : kSmemBlocks) : kRegBlocks;
 };
