@@ -364,7 +364,8 @@ def run_single(args, local):
         lf = {"value": lw * lsteps / lt, "unit": UNIT, "ms_per_step": 1e3 * lt / lsteps, "steps": lsteps,
               "roofline": roofline(args, lw, lt / lsteps, "lifetime", prof),
               "note": "reference default update order (ReuseMode::lifetime, sweep_samples trainer.cpp:133-154): "
-                      "K1s anti-diagonal wavefront"}
+                      "K1s window staircase (anti-diagonal wavefronts of consecutive windows overlapped, "
+                      "csrc/fw2v_stair.cuh)"}
         if not args.no_e2e:
             lf["e2e"] = e2e_leg(fw, args, corpus, "lifetime", local, lsteps)
         line["lifetime"] = lf
@@ -381,7 +382,8 @@ def config_block(args, shape, words, world, parallelism):
             "dim": args.dim, "window": args.window, "negatives": args.negatives, "subsample": 1e-4,
             "words_per_step_per_gpu": words, "batch_sentences": args.batch_sentences,
             "streams": args.streams, "chunks": args.chunks, "reuse_mode": args.reuse_mode,
-            "kernel": "K1s (FULL-W2V independent negatives, Hogwild)", "sampler": args.sampler,
+            "kernel": ("K1s (FULL-W2V independent negatives, Hogwild)" if args.reuse_mode == "window_snapshot"
+                       else "K1s window staircase (reference lifetime order, Hogwild)"), "sampler": args.sampler,
             "l1_refresh_log2": args.l1_refresh_log2,
             "deviations": {"hot_rows": (f"top {args.hot_rows} output rows trained as 16 replicas merged live (every "
                                         "replica's updates summed into the others every few microseconds by a resident "

@@ -190,8 +190,7 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     // g for a pairing with coefficient hn = valid ? -alpha/2 : 0 (label 1 for k = 0).
     auto coeff = [&](float f, float hn, bool positive) {
         if constexpr (FAST) {
-            const float h = fminf(fmaxf(0.5f * f, -3.0f), 3.0f);
-            return fmaf(hn, tanh_approx(h), positive ? -hn : hn);
+            return fmaf(hn, tanh_approx(half_clamped(f)), positive ? -hn : hn);
         } else {
             return sgd_coeff<false>(f, positive ? 1.0f : 0.0f, -2.0f * hn);
         }

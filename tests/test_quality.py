@@ -176,28 +176,41 @@ def test_text8_hot_band_loss(text8_reference, hot_rows):
     assert abs(gr - rr) / rr <= 0.02
 
 
+_OTHER = {}
+
+
+def _other_reference(ref, shape):
+    """The reference train() on one of the other shapes (cached per shape)."""
+    import os
+
+    if shape not in _OTHER:
+        s_exp, dim = (1.1, 128) if shape.startswith("zipf") else (1.0, 300)
+        c = fw.synth_zipf(types=fw.TEXT8_SHAPE["types"], tokens=fw.TEXT8_SHAPE["tokens"], s=s_exp)
+        cfg = dict(dim=dim, window=5, negatives=5, epochs=2, batch_sentences=10000, subsample=1e-4, seed=7)
+        rin, rout, _ = ref.train(c.counts, c.offsets, c.ids, RConfig(workers=os.cpu_count() or 8, **cfg))
+        _OTHER[shape] = (c, cfg, rin, rout)
+    return _OTHER[shape]
+
+
 @pytest.mark.parametrize("shape", ["zipf1.1_d128", "text8_d300"])
 @pytest.mark.parametrize("mode", ["window_snapshot", "lifetime"])
 def test_hogwild_quality_other_shapes(ref, shape, mode):
     """Two more distributions for the Hogwild budget and kernels:
     a steeper Zipf law (s = 1.1: hotter head rows, V_eff smaller) at d=128 and the
-    text8 law at d=300 (32 x 10 lane shape), 6,000 sentences, 3 epochs, the bench's
-    knobs with the automatic in-flight budget: SGNS loss within 2% of the
-    reference train() on all host cores."""
-    import os
-
-    s_exp, dim = (1.1, 128) if shape.startswith("zipf") else (1.0, 300)
-    c = fw.synth_zipf(types=fw.TEXT8_SHAPE["types"], tokens=fw.TEXT8_SHAPE["tokens"], s=s_exp).head(6000)
-    cfg = dict(dim=dim, window=5, negatives=5, epochs=3, batch_sentences=10000, subsample=1e-4, seed=7)
-    rin, rout, _ = ref.train(c.counts, c.offsets, c.ids, RConfig(workers=os.cpu_count() or 8, **cfg))
+    text8 law at d=300 (32 x 10 lane shape), the whole text8-sized corpus, 2 epochs,
+    the bench's knobs with the automatic in-flight budget: SGNS loss within 2% of
+    the reference train() on all host cores. (On a 6,000-sentence subset the
+    reference's own loss varied by 3% between runs of its Hogwild threads.)"""
+    c, cfg, rin, rout = _other_reference(ref, shape)
     with fw.Trainer(fw.TrainConfig(reuse_mode=mode, **cfg, **BENCH_KNOBS), c.counts) as t:
         t.train_corpus(c)
         gin, gout = t.get_model()
+    off = c.offsets[:2001].copy()
     p = c.counts.astype(np.float64) ** 0.75
-    negs = np.random.default_rng(5).choice(len(c.counts), len(c.ids) * 5, p=p / p.sum()).astype(np.int32)
+    negs = np.random.default_rng(5).choice(len(c.counts), int(off[-1]) * 5, p=p / p.sum()).astype(np.int32)
 
     def loss(i, o):
-        return sgns_loss(i, o, c.offsets, c.ids, negs, wf=3, n_neg=5, max_pairs=100_000)
+        return sgns_loss(i, o, off, c.ids[: int(off[-1])], negs, wf=3, n_neg=5, max_pairs=200_000)
 
     ref_loss, got = loss(rin, rout), loss(gin, gout)
     print(f"{shape} {mode}: loss {got:.4f} vs ref {ref_loss:.4f} ({100 * (got / ref_loss - 1):+.2f}%)")
