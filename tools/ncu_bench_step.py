@@ -18,7 +18,9 @@ shape = fw.TEXT8_SHAPE if workload == "text8" else fw.ONEBW_SHAPE
 corpus = fw.synth_zipf(**shape)
 cfg = fw.TrainConfig(dim=dim, window=5, negatives=5, epochs=2, workers=64, streams=16, batch_sentences=10000,
                      subsample=1e-4, seed=1, deterministic=0, reuse_mode=mode, sampler="alias", l1_refresh_log2=5,
-                     hot_rows=64)
+                     hot_rows=64, hot_merge=0)
+# (hot_merge=0: ncu serialises kernels, so the live merge block, which runs beside the
+# training kernels, would spin alone until its time cap; the K1s launches are the same.)
 cuda = C.CDLL("libcuda.so.1")
 with fw.Trainer(cfg, corpus.counts) as t:
     plan = t.plan_epoch(corpus, 0)

@@ -52,6 +52,8 @@ def main():
         dram = l2 = inst = t_all = t_k1s = 0.0
         n_k1s = 0
         for (_, name), m in rows.items():
+            if "k_hot_live" in name:  # the live merge runs beside the step; serialised it only spins
+                continue
             t = to_ns(*m["gpu__time_duration.sum"]) if "gpu__time_duration.sum" in m else 0.0
             t_all += t
             if "k1s" in name:
