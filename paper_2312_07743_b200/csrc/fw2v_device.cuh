@@ -48,6 +48,10 @@ struct ModelView {
     int32_t hot_k;
     int32_t hot_r;
     int32_t hot_row;  // (hot - syn1) / (stride floats): replica r of row id is syn1 row hot_row + r*hot_k + id
+    // Live hot-row merge: the training kernels count sentence starts here, so the
+    // merge block can tell a pass that is still training from one whose kernels
+    // cannot run beside it (a serialising profiler); null when not merging live.
+    unsigned int* beat = nullptr;
 };
 
 // K1s memory-path options.

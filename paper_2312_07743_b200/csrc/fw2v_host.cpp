@@ -767,7 +767,9 @@ struct fw2v_ctx {
         }
     }
     ModelView model_view() const {
-        return ModelView{syn0, syn1, cfg.dim, stride, vocab, k1_flags, hot, hot_k, hot_r, static_cast<int32_t>(hot_row)};
+        ModelView v{syn0, syn1, cfg.dim, stride, vocab, k1_flags, hot, hot_k, hot_r, static_cast<int32_t>(hot_row)};
+        v.beat = live() ? live_beat : nullptr;
+        return v;
     }
     // Around every Hogwild pass: replicas <- syn1 before, syn1 <- mean(replicas) after.
     void hot_sync(bool average, cudaStream_t st) const { FW2V_CK(launch_hot_sync(model_view(), average, st)); }
@@ -776,6 +778,7 @@ struct fw2v_ctx {
     cudaStream_t live_stream = nullptr;
     cudaEvent_t live_go = nullptr, live_done = nullptr;
     int* live_stop = nullptr;        // device flag
+    unsigned* live_beat = nullptr;   // sentence starts of the training kernels (ModelView::beat)
     int* live_started_h = nullptr;   // mapped host flag, set by the merge block
     int* live_started_d = nullptr;
     bool live() const { return cfg.hot_merge == 1 && hot_k > 0 && !deterministic; }
@@ -790,6 +793,8 @@ struct fw2v_ctx {
             FW2V_CK(cudaEventCreateWithFlags(&live_go, cudaEventDisableTiming));
             FW2V_CK(cudaEventCreateWithFlags(&live_done, cudaEventDisableTiming));
             FW2V_CK(cudaMalloc(&live_stop, sizeof(int)));
+            FW2V_CK(cudaMalloc(&live_beat, sizeof(unsigned)));
+            FW2V_CK(cudaMemset(live_beat, 0, sizeof(unsigned)));
             FW2V_CK(cudaHostAlloc(reinterpret_cast<void**>(&live_started_h), sizeof(int), cudaHostAllocMapped));
             FW2V_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&live_started_d), live_started_h, 0));
             // Every kernel the pass launches while the merge block runs is loaded now:
@@ -823,6 +828,10 @@ struct fw2v_ctx {
         }
         FW2V_CK(launch_set_flag(live_stop, st));
         FW2V_CK(cudaStreamWaitEvent(st, live_done, 0));
+        // One more sweep after every training kernel of the pass: the block may
+        // have left early (no sentence started for a while, e.g. under a profiler
+        // that serialises kernels); with the stop flag set it sweeps once and ends.
+        FW2V_CK(launch_hot_live(model_view(), live_stop, live_started_d, st));
     }
 
     Sampler sampler() const {
@@ -968,6 +977,7 @@ struct fw2v_ctx {
             cudaEventDestroy(live_go);
             cudaEventDestroy(live_done);
             cudaFree(live_stop);
+            cudaFree(live_beat);
             cudaFreeHost(live_started_h);
         }
         cudaFree(hot_alloc);

@@ -672,11 +672,21 @@ __global__ void __launch_bounds__(512) k_hot_live(ModelView m, const volatile in
     unsigned long long t0 = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     if (threadIdx.x == 0) *started = 1;
+    // Leaves when stopped, when no training sentence has started for kIdleNs (the
+    // pass's kernels are not running beside it: the host's final sweep catches up),
+    // or after max_ns (never outlive a lost stop).
+    constexpr unsigned long long kIdleNs = 20ull * 1000 * 1000;
+    unsigned seen = m.beat != nullptr ? *reinterpret_cast<volatile unsigned*>(m.beat) : 0u;
+    unsigned long long t_seen = t0;
     for (;;) {
         if (threadIdx.x == 0) {
             unsigned long long t = 0;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            last = (*stop != 0) || (t - t0 > max_ns);  // (time cap: never outlive a lost stop)
+            if (m.beat != nullptr) {
+                const unsigned b = *reinterpret_cast<volatile unsigned*>(m.beat);
+                if (b != seen) { seen = b; t_seen = t; }
+            }
+            last = (*stop != 0) || (t - t0 > max_ns) || (m.beat != nullptr && t - t_seen > kIdleNs);
         }
         __syncthreads();
         const bool fin = last != 0;
@@ -710,7 +720,7 @@ __global__ void __launch_bounds__(512) k_hot_live(ModelView m, const volatile in
 __global__ void k_set_flag(int* f) { *f = 1; }
 cudaError_t launch_hot_live(const ModelView& m, int* stop, int* started, cudaStream_t st) {
     if (m.hot_k <= 0 || m.hot_r > kMaxLiveReplicas) return cudaErrorInvalidValue;
-    k_hot_live<<<1, 512, 0, st>>>(m, stop, started, 2000u, 30ull * 1000 * 1000 * 1000);
+    k_hot_live<<<1, 512, 0, st>>>(m, stop, started, 2000u, 10ull * 1000 * 1000 * 1000);
     return cudaGetLastError();
 }
 cudaError_t launch_set_flag(int* f, cudaStream_t st) {

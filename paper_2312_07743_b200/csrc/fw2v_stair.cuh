@@ -100,6 +100,7 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     }
     const int L = static_cast<int>(len);
     if (sub == 0) obs_record_sentence(b, sent, L);  // observer (test mode)
+    if (m.beat != nullptr && threadIdx.x == 0) atomicAdd(m.beat, 1u);  // live merge: still training
     const int Lmax = static_cast<int>(__reduce_max_sync(kFull, len));
     if (Lmax == 0) return;
     const int32_t* __restrict__ ids = b.ids + beg;
