@@ -293,6 +293,29 @@ def e2e_leg(fw, args, corpus, mode, local, steps):
             "host_batching_words_per_sec_per_thread": rep.batching_words_per_sec, "batching_threads": args.streams}
 
 
+def configs_leg(fw, args, corpus, local):
+    """BASELINE.json configs[1] and [2] beside the headline: text8 at d=300 and the
+    1bw-shaped corpus (534 M trained words per epoch) at d=128, both update orders,
+    device-resident epochs on this GPU (the sweep, configs[4]: DESIGN.md section 6)."""
+    import copy
+
+    out = {}
+    d300 = copy.copy(args)
+    d300.dim = 300
+    for mode in ("window_snapshot", "lifetime"):
+        w, secs, _ = device_leg(fw, d300, corpus, mode, local, 5)
+        out[f"text8_d300_{mode}"] = {"value": w * 5 / sum(secs), "unit": UNIT, "words_per_step": w}
+    onebw = fw.synth_zipf(**fw.ONEBW_SHAPE)
+    for mode in ("window_snapshot", "lifetime"):
+        b = copy.copy(args)
+        b.workload = "1bw"
+        w, secs, _ = device_leg(fw, b, onebw, mode, local, 2)
+        out[f"1bw_d128_{mode}"] = {"value": w * 2 / sum(secs), "unit": UNIT, "words_per_step": w,
+                                   "roofline_frac": w * 2 / sum(secs) * algorithmic_bytes_per_word(128, args.negatives)
+                                   / 1e9 / load_peaks()[0]}
+    return out
+
+
 def dropin_leg(fw, args, corpus):
     """Whole ringvec::train calls through the C++ drop-in, reference default
     TrainConfig (workers = 0 -> hardware threads) except the bench's shape."""
@@ -371,6 +394,8 @@ def run_single(args, local):
         line["lifetime"] = lf
     if not args.no_dropin:
         line["dropin_e2e"] = dropin_leg(fw, args, corpus)
+    if not args.no_configs and args.workload == "text8" and args.dim == 128:
+        line["other_configs"] = configs_leg(fw, args, corpus, local)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args)
     print(json.dumps(line), flush=True)
@@ -569,6 +594,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-lifetime", action="store_true")
     ap.add_argument("--no-dropin", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the text8 d=300 and 1bw legs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world, rank, local, dist, shared = dist_setup()
