@@ -1170,7 +1170,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
             x->place_hot();
             x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
                                 : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives,
-                                                                         cfg->alpha0, x->live() ? 0 : x->hot_k, x->hot_r, cfg->dim)
+                                                                         cfg->alpha0, x->hot_k, x->hot_r, cfg->dim)
                                                          : 0;
         }
         if (x->inflight_total > 0 && !x->deterministic) {
