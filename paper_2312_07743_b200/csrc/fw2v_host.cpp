@@ -969,7 +969,7 @@ struct fw2v_ctx {
         cudaFree(d_words);
         cudaFree(merge_base);
         cudaFree(merge_cnt);
-        cudaFree(guard_snap);
+        BufferPool::get().put(guard_snap);
         cudaFree(guard_flag);
         if (live_stream) {
             cudaStreamSynchronize(live_stream);
@@ -982,8 +982,8 @@ struct fw2v_ctx {
         }
         cudaFree(hot_alloc);
         if (own_model) {
-            cudaFree(syn0);
-            cudaFree(syn1);
+            BufferPool::get().put(syn0);
+            BufferPool::get().put(syn1);
         }
     }
 };
@@ -1158,8 +1158,9 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
         if (cfg->sampler == FW2V_SAMPLER_ALIAS) x->alias.build(counts, vocab_size, cfg->table_power);
         require_device(cfg->device);
         const size_t bytes = sizeof(float) * static_cast<size_t>(vocab_size) * static_cast<size_t>(x->stride);
-        FW2V_CK(cudaMalloc(&x->syn0, bytes));
-        FW2V_CK(cudaMalloc(&x->syn1, bytes));
+        // (From the process-wide cache: a ringvec::train call creates one context.)
+        x->syn0 = static_cast<float*>(BufferPool::get().device(bytes));
+        x->syn1 = static_cast<float*>(BufferPool::get().device(bytes));
         Rng r = Rng::derive(cfg->seed, 0x696e6974ULL);  // "init" stream, model.cpp:26
         FW2V_CK(launch_init_model(x->model_view(), r.state, nullptr));
         FW2V_CK(cudaDeviceSynchronize());
@@ -1259,8 +1260,8 @@ int fw2v_attach_model(fw2v_ctx* x, float* syn0, float* syn1) {
         FW2V_CK(cudaSetDevice(x->cfg.device));
         FW2V_CK(cudaDeviceSynchronize());
         if (x->own_model) {
-            cudaFree(x->syn0);
-            cudaFree(x->syn1);
+            BufferPool::get().put(x->syn0);
+            BufferPool::get().put(x->syn1);
         }
         x->syn0 = syn0;
         x->syn1 = syn1;
@@ -1737,7 +1738,7 @@ constexpr int kGuardRetries = 4;
 void guard_save(fw2v_ctx* x) {
     const size_t n = x->model_floats();
     if (x->guard_snap == nullptr) {
-        FW2V_CK(cudaMalloc(&x->guard_snap, 2 * n * sizeof(float)));
+        x->guard_snap = static_cast<float*>(BufferPool::get().device(2 * n * sizeof(float)));
         FW2V_CK(cudaMalloc(&x->guard_flag, sizeof(int)));
     }
     FW2V_CK(cudaMemcpyAsync(x->guard_snap, x->syn0, n * sizeof(float), cudaMemcpyDeviceToDevice, nullptr));
