@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fw2v.h"
@@ -147,10 +148,21 @@ TrainResult train(const Corpus& corpus, const TrainConfig& raw_config, TrainObse
 
     std::vector<uint64_t> offsets(corpus.sentences.size() + 1, 0);
     for (size_t s = 0; s < corpus.sentences.size(); ++s) offsets[s + 1] = offsets[s] + corpus.sentences[s].length();
+    // Flattened on all host cores (67 MB for the text8 shape: ~20 ms on one).
     std::vector<int32_t> ids(offsets.back());
-    for (size_t s = 0; s < corpus.sentences.size(); ++s)
-        if (!corpus.sentences[s].ids.empty())
-            std::memcpy(ids.data() + offsets[s], corpus.sentences[s].ids.data(), sizeof(int32_t) * corpus.sentences[s].length());
+    {
+        const size_t ns = corpus.sentences.size();
+        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                for (size_t s = ns * t / nt; s < ns * (t + 1) / nt; ++s)
+                    if (!corpus.sentences[s].ids.empty())
+                        std::memcpy(ids.data() + offsets[s], corpus.sentences[s].ids.data(),
+                                    sizeof(int32_t) * corpus.sentences[s].length());
+            });
+        for (auto& x : th) x.join();
+    }
 
     Callbacks cb{observer, &on_epoch, {}};
     fw2v_report rep{};
