@@ -385,8 +385,6 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
         if (tok[r] >= 0) SL::load(ctx[r], syn0 + static_cast<int64_t>(tok[r]) * STRIDE); else vzero2(ctx[r]);
         if (delta_wb && r >= WF) SL::store_shared(ring + p * STRIDE, ctx[r]);  // p < C
     }
-    unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
-    unsigned s_rw = 0, pairs = 0;
 
     // Single-chunk path: every lane holds the negatives of windows i (ncur),
     // i+1 (nnext, for the prefetch) and, raw, i+2 (loaded one window early).
@@ -506,7 +504,6 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
             prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * n_neg);
             prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
         }
-        c_reads += inc_tok >= 0;
         if constexpr (MULTI && !LIFETIME) {
 #pragma unroll
             for (int r = 0; r < NCTX; ++r) vzero2(dctx[r]);
@@ -791,10 +788,6 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
 #pragma unroll
                 for (int h = 0; h < H2; ++h) ctx[r][h] = __fadd2_rn(ctx[r][h], dctx[r][h]);
         }
-        if (wact) {
-            s_rw += static_cast<unsigned>(n_neg + 1);
-            pairs += static_cast<unsigned>(__popc(vmask)) * static_cast<unsigned>(n_neg + 1);
-        }
 
         KB_T(7)
         // Slide the ring (ContextRing::advance, trainer.cpp:55-69).
@@ -880,6 +873,14 @@ __device__ __forceinline__ void k1s_sentence(const ModelView& m, const BatchView
 
     if (ctr != nullptr) {
         const bool lead = has && sub == 0;
+        // Closed forms of the per-window counts (each position read once; every
+        // window of a sentence of >= 2 words has N+1 samples and its valid contexts).
+        const unsigned ns = static_cast<unsigned>(n_neg + 1);
+        const unsigned c_reads = static_cast<unsigned>(L);
+        const unsigned s_rw = L >= 2 ? static_cast<unsigned>(L) * ns : 0u;
+        const unsigned half = L <= WF + 1 ? static_cast<unsigned>(L * (L - 1) / 2)
+                                          : static_cast<unsigned>(WF * (WF + 1) / 2 + (L - WF - 1) * WF);
+        const unsigned pairs = L >= 2 ? 2u * half * ns : 0u;
         const unsigned hits = (L >= 2) ? pairs - static_cast<unsigned>(L) : 0u;
         const unsigned v0 = __reduce_add_sync(kFull, lead ? c_reads : 0u);
         const unsigned v2 = __reduce_add_sync(kFull, lead ? s_rw : 0u);

@@ -124,8 +124,6 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
     unsigned qv = 0;  // bit r: Q[r] holds a position of the sentence
 #pragma unroll
     for (int r = 0; r < NQ; ++r) qv |= (qtok[r] >= 0 ? 1u : 0u) << r;
-    unsigned c_reads = static_cast<unsigned>(min(L, WF + 1));
-    unsigned s_rw = 0, pairs = 0;
 
     // Sample ids, one per lane: lane q (q = sub mod HALF < NC) of a group holds
     // sample q of a window (the target id for q = 0, negative q-1 otherwise),
@@ -276,7 +274,6 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
             prefetch_l2(negs + static_cast<size_t>(i + kPrefetchWindows) * NN);
             prefetch_l2(ids + min(L - 1, q_in + kPrefetchWindows));
         }
-        c_reads += inc_tok >= 0;
 
         const unsigned hvm = wact ? qv : 0u;  // head validity per ring row
 
@@ -373,10 +370,6 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
             tvm = 0;
         }
         stale_n = repeats(mm_n, dup_n);
-        if (wact) {
-            s_rw += NC;
-            pairs += static_cast<unsigned>(__popc(qv & ~(1u << WF))) * NC;
-        }
 
         // Slide the ring (ContextRing::advance, trainer.cpp:55-69): position
         // i - W_f leaves (its last pairing was window i's), i+1+W_f enters.
@@ -412,6 +405,13 @@ __device__ __forceinline__ void stair_sentence(const ModelView& m, const BatchVi
 
     if (ctr != nullptr) {
         const bool lead = has && sub == 0;
+        // Closed forms of the per-window counts (each position read once; every
+        // window of a sentence of >= 2 words has N+1 samples and its valid contexts).
+        const unsigned c_reads = static_cast<unsigned>(L);
+        const unsigned s_rw = L >= 2 ? static_cast<unsigned>(L) * NC : 0u;
+        const unsigned half = L <= WF + 1 ? static_cast<unsigned>(L * (L - 1) / 2)
+                                          : static_cast<unsigned>(WF * (WF + 1) / 2 + (L - WF - 1) * WF);
+        const unsigned pairs = L >= 2 ? 2u * half * NC : 0u;
         const unsigned hits = (L >= 2) ? pairs - static_cast<unsigned>(L) : 0u;
         const unsigned v0 = __reduce_add_sync(kFull, lead ? c_reads : 0u);
         const unsigned v2 = __reduce_add_sync(kFull, lead ? s_rw : 0u);
