@@ -1048,9 +1048,9 @@ int64_t auto_inflight(const uint64_t* counts, int32_t vocab_size, double power, 
     const double v_eff = z2 > 0.0 ? z * z / z2 : 1.0;
     // Wide rows tolerate less staleness (measured on the planted corpus: d=512 at
     // 888 sentences in flight +2.3% loss, at 512 +0.7%; d=128 fine at 3,552).
-    // Wide rows keep round 1's measured budget (8 x 0.025 scaled by (128/d)^2):
-    // at d=512 the planted corpus is +2.3% at 20 x 0.025 (tests/test_quality.py).
-    const double wide = dim > 128 ? 0.4 * (128.0 / dim) * (128.0 / dim) : 1.0;
+    // Above d=320 wide rows keep round 1's measured budget (8 x 0.025 scaled by
+    // (128/d)^2): at d=512 the planted corpus is +2.3% at 20 x 0.025.
+    const double wide = dim <= 128 ? 1.0 : (dim > 320 ? 0.4 : 1.0) * (128.0 / dim) * (128.0 / dim);
     const double m = 20.0 * 0.025 * v_eff / ((n_neg + 1) * static_cast<double>(alpha0)) * wide;
     return std::max<int64_t>(32, static_cast<int64_t>(std::ceil(m)));
 }
@@ -1171,7 +1171,7 @@ int fw2v_create(const fw2v_config* cfg, const uint64_t* counts, int32_t vocab_si
             x->place_hot();
             x->inflight_total = cfg->max_inflight > 0 ? cfg->max_inflight
                                 : cfg->max_inflight == 0 ? auto_inflight(counts, vocab_size, cfg->table_power, cfg->negatives,
-                                                                         cfg->alpha0, x->hot_k, x->hot_r, cfg->dim)
+                                                                         cfg->alpha0, x->live() ? 0 : x->hot_k, x->hot_r, cfg->dim)
                                                          : 0;
         }
         if (x->inflight_total > 0 && !x->deterministic) {
